@@ -1,0 +1,132 @@
+/*
+ * nvrec_b200.h -- C-ABI of the B200-native nvrec recovery path.
+ *
+ * One shared library (libnvrec_b200.so, sm_100a) exports plain-pointer
+ * entry points; no torch types cross this boundary.  Every function returns
+ * 0 on success or a negative NVREC_E* code; nvrec_last_error() then holds a
+ * message (thread-local).  Device pointers are caller-owned; nothing is
+ * allocated on the hot path (workspaces are sized by nvrec_workspace_bytes
+ * and passed in), and every launch goes to the caller's cudaStream_t, so the
+ * calls are CUDA-graph capturable.
+ *
+ * Reference interfaces replaced (arxiv 2604.27441, /root/reference/pkg):
+ *   nvrec_model_create/load  <- nvrec/train.py:40-43  Checkpoint.build_model
+ *                               + nn.Module.load_state_dict of
+ *                               nvrec/model.py:67-80  MaskedVideoModel.__init__
+ *   nvrec_forward_f32        <- nvrec/model.py:82-122 MaskedVideoModel.forward
+ *   nvrec_recover_u8         <- nvrec/server.py:181-196 RecoveryServer._recover
+ *                               (u8 stack/normalise, forward, quantise, merge)
+ *   nvrec_loss_mask          <- rgbdstream/receiver.py:224-237 zero-fill +
+ *                               rgbdstream/codec.py:159-201,250-257,274-281,
+ *                               318-320 (parse_header, block_ranges,
+ *                               _corrupted_blocks, decode mask) +
+ *                               rgbdstream/recovery.py:221 (wire bitset)
+ */
+#ifndef NVREC_B200_H
+#define NVREC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NVREC_ABI_VERSION 1
+
+enum {
+  NVREC_OK = 0,
+  NVREC_E_INVALID = -1,      /* bad argument (maps to ValueError)          */
+  NVREC_E_UNSUPPORTED = -2,  /* config the kernels do not implement        */
+  NVREC_E_CUDA = -3,         /* CUDA runtime / launch failure              */
+  NVREC_E_WORKSPACE = -4,    /* workspace too small                        */
+  NVREC_E_STATE = -5         /* weights not loaded                         */
+};
+
+/* Precision of the arithmetic on the forward path.
+ *   NVREC_PREC_FAST:    bf16 tensor-core (tcgen05) attention, fp32
+ *                       accumulation/softmax/LN/GELU; RGB and u8 depth.
+ *   NVREC_PREC_PRECISE: fp32 everywhere (CUDA-core SIMT); the 16-bit depth
+ *                       mode (<= 1/65535 of full scale). */
+enum { NVREC_PREC_FAST = 0, NVREC_PREC_PRECISE = 1 };
+
+/* Architecture fields of nvrec ModelConfig (config.py:14-19,35-41). */
+typedef struct nvrec_config {
+  int32_t k;          /* reference frames                                   */
+  int32_t tubelet_t;  /* frames per temporal token                          */
+  int32_t patch;      /* spatial patch edge (== mask block, 16)             */
+  int32_t dim;        /* token width                                        */
+  int32_t layers;     /* transformer blocks                                 */
+  int32_t heads;      /* attention heads                                    */
+} nvrec_config;
+
+typedef struct nvrec_model nvrec_model;   /* opaque; weights on one device */
+
+int nvrec_abi_version(void);
+const char* nvrec_last_error(void);
+
+/* Create a model for `channels` (3 = RGB, 1 = depth) on the current CUDA
+ * device.  Fails with NVREC_E_UNSUPPORTED for architectures outside the
+ * kernels' envelope (dim % 16, dim <= 128, dim/heads in {8,16,32,64}). */
+int nvrec_model_create(const nvrec_config* cfg, int32_t channels, nvrec_model** out);
+int nvrec_model_destroy(nvrec_model* m);
+
+/* Load fp32 HOST tensors in MaskedVideoModel state-dict order
+ * (time_pos, embed.weight, embed.bias, blocks.i.{norm_s, attn_s.qkv,
+ * attn_s.proj, norm_t, attn_t.qkv, attn_t.proj, norm_m, mlp.0, mlp.2}
+ * .{weight,bias}..., norm.weight, norm.bias, head.weight, head.bias).
+ * numel[i] is checked against the architecture.  Synchronous. */
+int nvrec_model_load(nvrec_model* m, const float* const* tensors,
+                     const int64_t* numel, int32_t n_tensors);
+
+/* Bytes of device workspace a forward/recover of this shape needs. */
+int64_t nvrec_workspace_bytes(const nvrec_model* m, int32_t batch,
+                              int32_t height, int32_t width, int32_t precision);
+
+/* MaskedVideoModel.forward: stack f32 (b, f, c, h, w) in [0,1] oldest first
+ * (f <= stack_len, front-padded with frame 0), mask u8 (b, h, w) nonzero =
+ * corrupted (any pixel pattern).  out f32 (b, c, h, w).  Device pointers. */
+int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b,
+                      int32_t f, int32_t c, int32_t h, int32_t w,
+                      const uint8_t* mask, float* out, void* workspace,
+                      int64_t workspace_bytes, int32_t precision, void* stream);
+
+/* RecoveryServer._recover over a batch of independent streams (block mask).
+ * frames: u8 planes (h, w, c) packed at `frames + slot * h*w*c`;
+ * frame_index: int32 (b, stack_len) slot of each stacked frame, oldest first,
+ *   already front-padded, the last entry the corrupted plane;
+ * mask_bits: u8 (b, ceil(gh*gw/8)) wire bitset (MSB-first, row-major);
+ * out: u8 (b, h, w, c) merged planes (unmasked pixels = corrupted plane).
+ * Only masked patches are decoded (exact: the merge discards the rest). */
+int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                     const uint8_t* frames, const int32_t* frame_index,
+                     const uint8_t* mask_bits, uint8_t* out, void* workspace,
+                     int64_t workspace_bytes, int32_t precision, void* stream);
+
+/* One P-frame's loss-mask job (all pointers are DEVICE pointers). */
+typedef struct nvrec_lossmask_job {
+  const uint8_t* header;      /* codec header bytes (shard 0 payload)        */
+  int32_t header_len;
+  int32_t n_data;             /* data shards incl. header shard 0            */
+  const uint8_t* received;    /* u8[n_data], nonzero = shard arrived         */
+  int32_t shard_len;          /* body shard payload length L                 */
+  int64_t body_len;           /* encoded_len - header_len (receiver.py:225)  */
+  int64_t payload_received;   /* len(assembled body); < payload_len => tail
+                                 zero-fill (codec.py:274-278)                */
+  const int64_t* extra_ranges;/* optional explicit [lo,hi) pairs or NULL     */
+  int32_t n_extra;
+  uint8_t* grid;              /* out u8[gh*gw] 0/1 (CorruptionMask.grid)     */
+  uint8_t* wire_bits;         /* out u8[ceil(gh*gw/8)] (np.packbits) or NULL */
+  int32_t* status;            /* out: 0 ok, else UndecodableError reason;
+                                 [1] = flagged count, [2] = gh, [3] = gw     */
+  int32_t grid_capacity;      /* bytes available at grid                    */
+} nvrec_lossmask_job;
+
+/* Batched loss-mask kernel: jobs is a DEVICE array of n_jobs descriptors.
+ * Bit-exact with the reference receiver+codec. */
+int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NVREC_B200_H */

@@ -1,0 +1,458 @@
+// capi.cu -- the C-ABI (include/nvrec_b200.h): model objects, weight
+// packing, workspace carve-up and the per-forward launch sequence.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cstdarg>
+#include <cmath>
+
+#include "launch.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NVREC_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                  \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, what);  \
+  } while (0)
+
+}  // namespace
+
+struct nvrec_model {
+  nvrec_config cfg;
+  nvrec::Dims D;
+  int device = 0;
+  float* blob = nullptr;        // all packed fp32 weights
+  size_t blob_floats = 0;
+  nvrec::ModelW W{};
+  bool loaded = false;
+};
+
+namespace {
+
+using nvrec::Dims;
+
+Dims make_dims(const nvrec_config& c, int channels) {
+  Dims D;
+  D.c = channels;
+  D.d = c.dim;
+  D.heads = c.heads;
+  D.hd = c.dim / c.heads;
+  D.T = c.tubelet_t;
+  D.p = c.patch;
+  int raw = c.k + 1;
+  D.F = raw + ((c.tubelet_t - raw % c.tubelet_t) % c.tubelet_t);
+  D.nt = D.F / D.T;
+  D.layers = c.layers;
+  D.hidden = 4 * c.dim;
+  D.kimg = channels * D.T * D.p * D.p;
+  D.used = D.p * D.p * channels;
+  return D;
+}
+
+// expected numel of each state-dict tensor, in state-dict order
+std::vector<int64_t> expected_numel(const Dims& D) {
+  std::vector<int64_t> v;
+  const int64_t d = D.d;
+  v.push_back(int64_t(D.nt) * d);                                  // time_pos
+  v.push_back(d * (D.c + 1) * D.T * D.p * D.p);                    // embed.weight
+  v.push_back(d);                                                  // embed.bias
+  for (int i = 0; i < D.layers; ++i) {
+    const int64_t blk[18] = {d, d, 3 * d * d, 3 * d, d * d, d,     // norm_s, attn_s
+                             d, d, 3 * d * d, 3 * d, d * d, d,     // norm_t, attn_t
+                             d, d, 4 * d * d, 4 * d, 4 * d * d, d};// norm_m, mlp
+    v.insert(v.end(), blk, blk + 18);
+  }
+  v.push_back(d);
+  v.push_back(d);                                                  // norm
+  v.push_back(int64_t(D.T) * D.p * D.p * D.c * d);                 // head.weight
+  v.push_back(int64_t(D.T) * D.p * D.p * D.c);                     // head.bias
+  return v;
+}
+
+// nn.Linear weight (out, in) -> K-major [in][out]
+void transpose_into(std::vector<float>& dst, const float* w, int out, int in) {
+  for (int k = 0; k < in; ++k)
+    for (int n = 0; n < out; ++n) dst.push_back(w[size_t(n) * in + k]);
+}
+
+struct WorkspaceLayout {
+  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, total;
+};
+
+WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
+  const int ns = (h / D.p) * (w / D.p);
+  const int ns_pad = nvrec::round_up(ns, nvrec::kAttnQTile);
+  WorkspaceLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t tok = size_t(b) * D.nt * ns;
+  const size_t seqrows = size_t(b) * D.nt * D.heads * ns_pad * D.hd;
+  L.x = take(tok * D.d * 4);
+  L.ao = take(tok * D.d * 4);
+  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(D);
+  if (fast) {
+    L.qh = take(seqrows * 2);
+    L.kh = take(seqrows * 2);
+    L.vth = take(seqrows * 2);
+    L.q = L.k = L.v = SIZE_MAX;
+  } else {
+    L.q = take(seqrows * 4);
+    L.k = take(seqrows * 4);
+    L.v = take(seqrows * 4);
+    L.qh = L.kh = L.vth = SIZE_MAX;
+  }
+  L.list = take(size_t(b) * ns * 4);
+  L.rank = take(size_t(b) * ns * 4);
+  L.count = take(size_t(b) * 4);
+  L.total = off;
+  return L;
+}
+
+template <class T>
+T* at(void* base, size_t off) {
+  return off == SIZE_MAX ? nullptr : reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+int check_arch(const nvrec_config* cfg, int channels) {
+  if (!cfg) return fail(NVREC_E_INVALID, "null config");
+  if (channels != 1 && channels != 3) return fail(NVREC_E_INVALID, "channels must be 1 or 3");
+  if (cfg->k < 1 || cfg->tubelet_t < 1 || cfg->patch < 1 || cfg->dim < 1 ||
+      cfg->layers < 1 || cfg->heads < 1 || cfg->dim % cfg->heads)
+    return fail(NVREC_E_INVALID, "invalid ModelConfig");
+  const int hd = cfg->dim / cfg->heads;
+  if (cfg->dim % 16 || cfg->dim > nvrec::kMaxDim || !(hd == 8 || hd == 16 || hd == 32 || hd == 64))
+    return fail(NVREC_E_UNSUPPORTED, "unsupported dim/heads (dim %% 16 == 0, dim <= 128, "
+                "dim/heads in {8,16,32,64}); got dim=%d heads=%d", cfg->dim, cfg->heads);
+  if (cfg->layers > 8) return fail(NVREC_E_UNSUPPORTED, "layers > 8 unsupported");
+  int raw = cfg->k + 1;
+  int F = raw + ((cfg->tubelet_t - raw % cfg->tubelet_t) % cfg->tubelet_t);
+  if (F / cfg->tubelet_t > nvrec::kMaxNt) return fail(NVREC_E_UNSUPPORTED, "too many time slices");
+  if ((cfg->patch * cfg->patch * channels) % 4)
+    return fail(NVREC_E_UNSUPPORTED, "patch*patch*channels must be a multiple of 4");
+  return 0;
+}
+
+// Shared launch sequence after the embedding: blocks, attention, head.
+int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bool fast,
+               bool pruned, int h, int w, float* out_f32, uint8_t* out_u8,
+               cudaStream_t s) {
+  const Dims& D = m->D;
+  const int b = A.b;
+  nvrec::QkvDst dst{};
+  dst.nt = D.nt; dst.ns = A.ns; dst.ns_pad = A.ns_pad; dst.d = D.d;
+  dst.heads = D.heads; dst.hd = D.hd;
+  dst.q = A.q; dst.k = A.k; dst.v = A.v; dst.qh = A.qh; dst.kh = A.kh; dst.vth = A.vth;
+  for (int li = 0; li < D.layers; ++li) {
+    const bool last = li == D.layers - 1;
+    const bool prune_here = last && pruned;
+    // block li's spatial attention: Q/K/V were written by the previous stage
+    cudaError_t e;
+    if (fast) {
+      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s);
+    } else {
+      nvrec::AttnArgs aa{};
+      aa.q = A.q; aa.k = A.k; aa.v = A.v; aa.ao = A.ao;
+      aa.count = prune_here ? A.count : nullptr;
+      aa.nt = D.nt; aa.heads = D.heads; aa.ns = A.ns; aa.ns_pad = A.ns_pad; aa.d = D.d;
+      aa.scale_log2 = 1.4426950408889634f / sqrtf(float(D.hd));
+      e = nvrec::launch_attn_simt(aa, b, A.ns, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "spatial attention launch");
+    nvrec::TokenArgs ta{};
+    ta.D = D;
+    ta.w = m->W.blk[li];
+    if (!last) ta.wn = m->W.blk[li + 1];
+    ta.norm_w = m->W.norm_w; ta.norm_b = m->W.norm_b;
+    ta.head_w = m->W.head_w; ta.head_b = m->W.head_b;
+    ta.last = last;
+    ta.list = prune_here ? A.list : nullptr;
+    ta.count = A.count;
+    ta.x = A.x; ta.ao = A.ao;
+    ta.dst = dst;
+    // the next block is the last: its Q rows are compact when pruned
+    ta.dst.rank = (!last && li + 1 == D.layers - 1 && pruned) ? A.rank : nullptr;
+    ta.img_h = h; ta.img_w = w; ta.nh = A.nh; ta.nw = A.nw; ta.ns = A.ns;
+    ta.out_f32 = out_f32; ta.out_u8 = out_u8;
+    e = nvrec::launch_token(ta, b, A.ns, s);
+    if (e != cudaSuccess) return cuda_fail(e, "token kernel launch");
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nvrec_abi_version(void) { return NVREC_ABI_VERSION; }
+const char* nvrec_last_error(void) { return g_err.c_str(); }
+
+int nvrec_model_create(const nvrec_config* cfg, int32_t channels, nvrec_model** out) {
+  if (!out) return fail(NVREC_E_INVALID, "null out");
+  int rc = check_arch(cfg, channels);
+  if (rc) return rc;
+  nvrec_model* m = new nvrec_model();
+  m->cfg = *cfg;
+  m->D = make_dims(*cfg, channels);
+  cudaGetDevice(&m->device);
+  *out = m;
+  return 0;
+}
+
+int nvrec_model_destroy(nvrec_model* m) {
+  if (!m) return 0;
+  if (m->blob) cudaFree(m->blob);
+  delete m;
+  return 0;
+}
+
+int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel,
+                     int32_t n) {
+  if (!m || !t || !numel) return fail(NVREC_E_INVALID, "null argument");
+  const Dims& D = m->D;
+  std::vector<int64_t> want = expected_numel(D);
+  if (n != int(want.size()))
+    return fail(NVREC_E_INVALID, "expected %d state tensors, got %d", int(want.size()), n);
+  for (int i = 0; i < n; ++i)
+    if (numel[i] != want[i])
+      return fail(NVREC_E_INVALID, "state tensor %d has %lld elements, expected %lld", i,
+                  (long long)numel[i], (long long)want[i]);
+  const int d = D.d, p = D.p, c = D.c, T = D.T;
+  std::vector<float> h;
+  std::vector<size_t> off;
+  auto mark = [&]() { off.push_back(h.size()); };
+  // embed: W[o][ci][tt][py][px] -> [((tt*p+py)*p+px)*c+ci][o]
+  const float* ew = t[1];
+  auto ew_at = [&](int o, int ci, int tt, int py, int px) {
+    return ew[((((size_t)o * (c + 1) + ci) * T + tt) * p + py) * p + px];
+  };
+  mark();  // 0 emb_w
+  for (int tt = 0; tt < T; ++tt)
+    for (int py = 0; py < p; ++py)
+      for (int px = 0; px < p; ++px)
+        for (int ci = 0; ci < c; ++ci)
+          for (int o = 0; o < d; ++o) h.push_back(ew_at(o, ci, tt, py, px));
+  mark();  // 1 emb_wmask [p*p][d] at tt = T-1, channel c
+  for (int py = 0; py < p; ++py)
+    for (int px = 0; px < p; ++px)
+      for (int o = 0; o < d; ++o) h.push_back(ew_at(o, c, T - 1, py, px));
+  mark();  // 2 emb_wmsum
+  for (int o = 0; o < d; ++o) {
+    float sacc = 0.f;
+    for (int py = 0; py < p; ++py)
+      for (int px = 0; px < p; ++px) sacc += ew_at(o, c, T - 1, py, px);
+    h.push_back(sacc);
+  }
+  mark();  // 3 emb_b
+  h.insert(h.end(), t[2], t[2] + d);
+  mark();  // 4 time_pos
+  h.insert(h.end(), t[0], t[0] + size_t(D.nt) * d);
+  std::vector<size_t> blk_off;
+  for (int i = 0; i < D.layers; ++i) {
+    const float* const* bt = t + 3 + 18 * i;
+    // order inside BlockW: ln_s_w, ln_s_b, qkv_s_w, qkv_s_b, proj_s_w, proj_s_b,
+    //   ln_t_w, ln_t_b, qkv_t_w, qkv_t_b, proj_t_w, proj_t_b,
+    //   ln_m_w, ln_m_b, fc1_w, fc1_b, fc2_w, fc2_b
+    const int outs[18] = {0, 0, 3 * d, 0, d, 0, 0, 0, 3 * d, 0, d, 0, 0, 0, 4 * d, 0, d, 0};
+    const int ins[18] = {0, 0, d, 0, d, 0, 0, 0, d, 0, d, 0, 0, 0, d, 0, 4 * d, 0};
+    for (int j = 0; j < 18; ++j) {
+      blk_off.push_back(h.size());
+      if (outs[j]) transpose_into(h, bt[j], outs[j], ins[j]);
+      else h.insert(h.end(), bt[j], bt[j] + want[3 + 18 * i + j]);
+      while (h.size() % 4) h.push_back(0.f);   // keep float4 alignment
+    }
+  }
+  const int tail = 3 + 18 * D.layers;
+  mark();  // 5 norm_w
+  h.insert(h.end(), t[tail], t[tail] + d);
+  mark();  // 6 norm_b
+  h.insert(h.end(), t[tail + 1], t[tail + 1] + d);
+  // head: keep rows ((T-1)*p*p + py*p + px)*c + ch (model.py:119-120), K-major
+  mark();  // 7 head_w [d][used]
+  const float* hw = t[tail + 2];
+  const size_t base_row = size_t(T - 1) * p * p * c;
+  for (int k = 0; k < d; ++k)
+    for (int u = 0; u < D.used; ++u) h.push_back(hw[(base_row + u) * d + k]);
+  mark();  // 8 head_b
+  for (int u = 0; u < D.used; ++u) h.push_back(t[tail + 3][base_row + u]);
+
+  if (m->blob) { cudaFree(m->blob); m->blob = nullptr; }
+  CK(cudaSetDevice(m->device), "cudaSetDevice");
+  CK(cudaMalloc(&m->blob, h.size() * sizeof(float)), "cudaMalloc(weights)");
+  CK(cudaMemcpy(m->blob, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice),
+     "cudaMemcpy(weights)");
+  m->blob_floats = h.size();
+  float* B = m->blob;
+  m->W.emb_w = B + off[0];
+  m->W.emb_wmask = B + off[1];
+  m->W.emb_wmsum = B + off[2];
+  m->W.emb_b = B + off[3];
+  m->W.time_pos = B + off[4];
+  for (int i = 0; i < D.layers; ++i) {
+    const float* p18[18];
+    for (int j = 0; j < 18; ++j) p18[j] = B + blk_off[18 * i + j];
+    nvrec::BlockW& bw = m->W.blk[i];
+    bw.ln_s_w = p18[0]; bw.ln_s_b = p18[1]; bw.qkv_s_w = p18[2]; bw.qkv_s_b = p18[3];
+    bw.proj_s_w = p18[4]; bw.proj_s_b = p18[5];
+    bw.ln_t_w = p18[6]; bw.ln_t_b = p18[7]; bw.qkv_t_w = p18[8]; bw.qkv_t_b = p18[9];
+    bw.proj_t_w = p18[10]; bw.proj_t_b = p18[11];
+    bw.ln_m_w = p18[12]; bw.ln_m_b = p18[13]; bw.fc1_w = p18[14]; bw.fc1_b = p18[15];
+    bw.fc2_w = p18[16]; bw.fc2_b = p18[17];
+  }
+  m->W.norm_w = B + off[5];
+  m->W.norm_b = B + off[6];
+  m->W.head_w = B + off[7];
+  m->W.head_b = B + off[8];
+  m->loaded = true;
+  return 0;
+}
+
+int64_t nvrec_workspace_bytes(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                              int32_t precision) {
+  if (!m || b < 1 || h < 1 || w < 1) return fail(NVREC_E_INVALID, "bad shape");
+  return int64_t(layout_ws(m->D, b, h, w, precision).total);
+}
+
+static int common_checks(const nvrec_model* m, int b, int h, int w, void* ws,
+                         int64_t ws_bytes, int precision, WorkspaceLayout* L) {
+  if (!m) return fail(NVREC_E_INVALID, "null model");
+  if (!m->loaded) return fail(NVREC_E_STATE, "weights not loaded");
+  if (b < 1) return fail(NVREC_E_INVALID, "batch must be >= 1");
+  if (h % m->D.p || w % m->D.p || h < 1 || w < 1)
+    return fail(NVREC_E_INVALID, "frame size must be a multiple of the patch edge");
+  if (precision != NVREC_PREC_FAST && precision != NVREC_PREC_PRECISE)
+    return fail(NVREC_E_INVALID, "unknown precision %d", precision);
+  *L = layout_ws(m->D, b, h, w, precision);
+  if (!ws || ws_bytes < int64_t(L->total))
+    return fail(NVREC_E_WORKSPACE, "workspace too small: %lld < %lld", (long long)ws_bytes,
+                (long long)L->total);
+  return 0;
+}
+
+static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout& L, int b,
+                           int h, int w) {
+  nvrec::Act A{};
+  A.x = at<float>(ws, L.x);
+  A.ao = at<float>(ws, L.ao);
+  A.q = at<float>(ws, L.q);
+  A.k = at<float>(ws, L.k);
+  A.v = at<float>(ws, L.v);
+  A.qh = at<__nv_bfloat16>(ws, L.qh);
+  A.kh = at<__nv_bfloat16>(ws, L.kh);
+  A.vth = at<__nv_bfloat16>(ws, L.vth);
+  A.list = at<int>(ws, L.list);
+  A.rank = at<int>(ws, L.rank);
+  A.count = at<int>(ws, L.count);
+  A.b = b;
+  A.nh = h / m->D.p;
+  A.nw = w / m->D.p;
+  A.ns = A.nh * A.nw;
+  A.ns_pad = nvrec::round_up(A.ns, nvrec::kAttnQTile);
+  return A;
+}
+
+static int embed_and_qkv0(const nvrec_model* m, nvrec::Act& A, bool u8, const float* stack,
+                          int f, const uint8_t* pmask, const uint8_t* frames,
+                          const int32_t* frame_index, int h, int w, bool pruned,
+                          cudaStream_t s) {
+  const Dims& D = m->D;
+  nvrec::EmbedArgs ea{};
+  ea.D = D;
+  ea.emb_w = m->W.emb_w; ea.emb_wmask = m->W.emb_wmask; ea.emb_wmsum = m->W.emb_wmsum;
+  ea.emb_b = m->W.emb_b; ea.time_pos = m->W.time_pos;
+  ea.frames = frames; ea.frame_index = frame_index;
+  ea.frame_bytes = size_t(h) * w * D.c;
+  ea.rank = u8 ? A.rank : nullptr;
+  ea.stack = stack; ea.f_in = f; ea.pmask = pmask;
+  ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns;
+  ea.x = A.x;
+  cudaError_t e = nvrec::launch_embed(ea, u8, A.b, s);
+  if (e != cudaSuccess) return cuda_fail(e, "embed launch");
+  nvrec::LnQkvArgs la{};
+  la.D = D;
+  la.x = A.x;
+  la.ln_w = m->W.blk[0].ln_s_w; la.ln_b = m->W.blk[0].ln_s_b;
+  la.qkv_w = m->W.blk[0].qkv_s_w; la.qkv_b = m->W.blk[0].qkv_s_b;
+  la.dst.q = A.q; la.dst.k = A.k; la.dst.v = A.v;
+  la.dst.qh = A.qh; la.dst.kh = A.kh; la.dst.vth = A.vth;
+  la.dst.rank = (pruned && D.layers == 1) ? A.rank : nullptr;
+  la.dst.nt = D.nt; la.dst.ns = A.ns; la.dst.ns_pad = A.ns_pad; la.dst.d = D.d;
+  la.dst.heads = D.heads; la.dst.hd = D.hd;
+  la.ns = A.ns;
+  e = nvrec::launch_ln_qkv(la, A.b, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ln_qkv launch");
+  return 0;
+}
+
+int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b, int32_t f,
+                      int32_t c, int32_t h, int32_t w, const uint8_t* mask, float* out,
+                      void* ws, int64_t ws_bytes, int32_t precision, void* stream) {
+  if (m && c != m->D.c)
+    return fail(NVREC_E_INVALID, "expected %d channels, got %d", m->D.c, c);
+  WorkspaceLayout L;
+  int rc = common_checks(m, b, h, w, ws, ws_bytes, precision, &L);
+  if (rc) return rc;
+  if (f < 1 || f > m->D.F) return fail(NVREC_E_INVALID, "stack longer than configured length");
+  if (!stack || !mask || !out) return fail(NVREC_E_INVALID, "null tensor pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  nvrec::Act A = make_act(m, ws, L, b, h, w);
+  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
+  rc = embed_and_qkv0(m, A, false, stack, f, mask, nullptr, nullptr, h, w, false, s);
+  if (rc) return rc;
+  return run_blocks(m, A, L, fast, false, h, w, out, nullptr, s);
+}
+
+int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                     const uint8_t* frames, const int32_t* frame_index,
+                     const uint8_t* mask_bits, uint8_t* out, void* ws, int64_t ws_bytes,
+                     int32_t precision, void* stream) {
+  WorkspaceLayout L;
+  int rc = common_checks(m, b, h, w, ws, ws_bytes, precision, &L);
+  if (rc) return rc;
+  if (m->D.p != 16)
+    return fail(NVREC_E_UNSUPPORTED, "u8 recover path needs patch == mask block (16)");
+  if (!frames || !frame_index || !mask_bits || !out)
+    return fail(NVREC_E_INVALID, "null pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  nvrec::Act A = make_act(m, ws, L, b, h, w);
+  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
+  const int nbytes = (A.ns + 7) / 8;
+  cudaError_t e = nvrec::launch_masklist(mask_bits, b, nbytes, A.ns, A.list, A.rank, A.count, s);
+  if (e != cudaSuccess) return cuda_fail(e, "masklist launch");
+  e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
+  if (e != cudaSuccess) return cuda_fail(e, "copy launch");
+  rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
+  if (rc) return rc;
+  return run_blocks(m, A, L, fast, true, h, w, nullptr, out, s);
+}
+
+int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(NVREC_E_INVALID, "bad job array");
+  cudaError_t e = nvrec::launch_lossmask(jobs, n_jobs, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "loss-mask launch");
+  return 0;
+}
+
+}  // extern "C"

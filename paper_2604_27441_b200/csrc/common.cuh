@@ -1,0 +1,83 @@
+// common.cuh -- shared definitions for the nvrec B200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "nvrec_b200.h"
+
+namespace nvrec {
+
+constexpr int kMaxDim = 128;
+constexpr int kMaxNt = 16;
+constexpr int kAttnQTile = 128;     // queries per attention CTA / key padding unit
+
+// Model geometry derived from nvrec ModelConfig + channels
+// (model.py:70-80; config.py:35-41).
+struct Dims {
+  int c;        // image channels (3 RGB / 1 depth)
+  int d;        // dim
+  int heads, hd;
+  int T, p;     // tubelet frames, patch edge
+  int F, nt;    // stack_len, time slices
+  int layers;
+  int hidden;   // 4*d
+  int kimg;     // c*T*p*p   (image part of the embed contraction)
+  int used;     // p*p*c     (head columns of the last tubelet frame)
+};
+
+// Per-block weights, all fp32, weight matrices stored K-major ("Wt[k][n]",
+// the transpose of nn.Linear's (out, in)), so a warp reading one k row for
+// consecutive n is coalesced.
+struct BlockW {
+  const float *ln_s_w, *ln_s_b, *qkv_s_w, *qkv_s_b, *proj_s_w, *proj_s_b;
+  const float *ln_t_w, *ln_t_b, *qkv_t_w, *qkv_t_b, *proj_t_w, *proj_t_b;
+  const float *ln_m_w, *ln_m_b, *fc1_w, *fc1_b, *fc2_w, *fc2_b;
+};
+
+struct ModelW {
+  const float* emb_w;      // [kimg][d], k = ((tt*p+py)*p+px)*c+ci
+  const float* emb_wmask;  // [p*p][d] mask-channel weights at tt = T-1
+  const float* emb_wmsum;  // [d]      sum of emb_wmask over pixels
+  const float* emb_b;      // [d]
+  const float* time_pos;   // [nt][d]
+  BlockW blk[8];
+  const float* norm_w;
+  const float* norm_b;
+  const float* head_w;     // [d][used] last-tubelet-frame columns only
+  const float* head_b;     // [used]
+};
+
+// Token-stream buffers of one forward (workspace carve-up).
+struct Act {
+  float* x;          // [b][nt][ns][d] residual stream
+  float* ao;         // [b][nt][nrow][d] spatial-attention output (compact rows
+                     //   when `list` is set: row r <-> list[r])
+  float* q;          // f32 path: [b*nt*heads][nq_pad][hd]; rows compact when
+  float* k;          //   the consuming block is pruned
+  float* v;          // [b*nt*heads][ns_pad][hd]
+  __nv_bfloat16* qh; // bf16 path: Q,K [seq][ns_pad][32]; Vt [seq][32][ns_pad]
+  __nv_bfloat16* kh;
+  __nv_bfloat16* vth;
+  int* list;         // [b][ns] masked positions (ascending) or nullptr = dense
+  int* rank;         // [b][ns] position -> row in list, -1 if absent
+  int* count;        // [b] entries in list
+  int b, ns, nh, nw, ns_pad;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int round_up(int a, int b) { return ceil_div(a, b) * b; }
+
+}  // namespace nvrec

@@ -1,0 +1,76 @@
+// launch.cuh -- kernel argument blocks and host launchers shared between the
+// kernel translation units and the C-ABI (capi.cu).
+#pragma once
+
+#include "tile_ops.cuh"
+
+namespace nvrec {
+
+struct EmbedArgs {
+  Dims D;
+  const float* emb_w;      // [kimg][d]
+  const float* emb_wmask;  // [p*p][d]
+  const float* emb_wmsum;  // [d]
+  const float* emb_b;      // [d]
+  const float* time_pos;   // [nt][d]
+  // U8 path
+  const uint8_t* frames;
+  const int32_t* frame_index;  // [b][F]
+  size_t frame_bytes;
+  const int* rank;             // [b][ns] >= 0 <=> patch masked
+  // F32 path
+  const float* stack;          // (b, f_in, c, h, w)
+  int f_in;
+  const uint8_t* pmask;        // (b, h, w)
+  int h, w, nh, nw, ns;
+  float* x;                    // [b][nt][ns][d]
+};
+
+struct LnQkvArgs {
+  Dims D;
+  const float* x;
+  const float* ln_w; const float* ln_b; const float* qkv_w; const float* qkv_b;
+  QkvDst dst;
+  int ns;
+};
+
+struct TokenArgs {
+  Dims D;
+  BlockW w;             // this block
+  BlockW wn;            // next block (ln_s/qkv_s used) when !last
+  const float* norm_w; const float* norm_b;
+  const float* head_w; const float* head_b;
+  int last;
+  const int* list;      // masked positions (ascending) or null = dense
+  const int* count;
+  float* x;             // [b][nt][ns][d]
+  const float* ao;      // [b][nt][ns][d], row r (compact when list)
+  QkvDst dst;           // next block's Q/K/V
+  int img_h, img_w, nh, nw, ns;
+  float* out_f32;       // (b, c, h, w) or null
+  uint8_t* out_u8;      // (b, h, w, c) or null
+};
+
+struct AttnArgs {
+  const float* q; const float* k; const float* v;
+  float* ao;              // [b][nt][ns][d] rows r
+  const int* count;       // compact query count per stream or null (= ns)
+  int nt, heads, ns, ns_pad, d;
+  float scale_log2;       // log2(e) / sqrt(hd)
+};
+
+// tensor-core spatial attention envelope (k_attn_tc.cu)
+bool tc_supported(const Dims& D);
+
+cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s);
+cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s);
+cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index, int F,
+                              size_t frame_bytes, uint8_t* out, int b, cudaStream_t s);
+cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s);
+cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_t s);
+cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s);
+cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
+cudaError_t launch_masklist(const uint8_t* bits, int b, int nbytes, int ns, int* list,
+                            int* rank, int* count, cudaStream_t s);
+
+}  // namespace nvrec

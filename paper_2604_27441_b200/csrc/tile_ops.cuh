@@ -1,0 +1,130 @@
+// tile_ops.cuh -- CTA-level fp32 building blocks shared by the token kernels:
+// small GEMMs against K-major weights, LayerNorm, and the Q/K/V scatter into
+// the spatial-attention layouts.
+#pragma once
+
+#include "common.cuh"
+
+namespace nvrec {
+
+// out(t, n) = sum_k in[t*ldi + k] * Wt[k*N + n] + bias[n], for t < ntok,
+// n < N (N % 4 == 0).  `in` lives in shared memory; Wt/bias in global (L1/L2
+// resident: the whole model is ~1.5 MB).  Each work item is a 4-token x
+// 4-column register tile: per k one 16-byte coalesced weight load, four
+// broadcast shared loads and 16 FMAs.  epi(t, n, v) consumes each result.
+template <class Epi>
+__device__ __forceinline__ void tile_gemm(const float* in, int ldi, int ntok, int K,
+                                          const float* __restrict__ Wt,
+                                          const float* __restrict__ bias, int N,
+                                          Epi epi) {
+  const int nq = N >> 2;
+  const int tq = (ntok + 3) >> 2;
+  for (int item = threadIdx.x; item < nq * tq; item += blockDim.x) {
+    const int cq = item % nq, tg = item / nq;
+    const int t0 = tg * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    const float* a0 = in + min(t0 + 0, ntok - 1) * ldi;
+    const float* a1 = in + min(t0 + 1, ntok - 1) * ldi;
+    const float* a2 = in + min(t0 + 2, ntok - 1) * ldi;
+    const float* a3 = in + min(t0 + 3, ntok - 1) * ldi;
+    const float* w = Wt + cq * 4;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + size_t(k) * N));
+      const float x0 = a0[k], x1 = a1[k], x2 = a2[k], x3 = a3[k];
+      acc[0][0] = fmaf(x0, wv.x, acc[0][0]); acc[0][1] = fmaf(x0, wv.y, acc[0][1]);
+      acc[0][2] = fmaf(x0, wv.z, acc[0][2]); acc[0][3] = fmaf(x0, wv.w, acc[0][3]);
+      acc[1][0] = fmaf(x1, wv.x, acc[1][0]); acc[1][1] = fmaf(x1, wv.y, acc[1][1]);
+      acc[1][2] = fmaf(x1, wv.z, acc[1][2]); acc[1][3] = fmaf(x1, wv.w, acc[1][3]);
+      acc[2][0] = fmaf(x2, wv.x, acc[2][0]); acc[2][1] = fmaf(x2, wv.y, acc[2][1]);
+      acc[2][2] = fmaf(x2, wv.z, acc[2][2]); acc[2][3] = fmaf(x2, wv.w, acc[2][3]);
+      acc[3][0] = fmaf(x3, wv.x, acc[3][0]); acc[3][1] = fmaf(x3, wv.y, acc[3][1]);
+      acc[3][2] = fmaf(x3, wv.z, acc[3][2]); acc[3][3] = fmaf(x3, wv.w, acc[3][3]);
+    }
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(bias + cq * 4));
+    const float bb[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (t0 + i < ntok) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) epi(t0 + i, cq * 4 + j, acc[i][j] + bb[j]);
+      }
+    }
+  }
+}
+
+// LayerNorm (eps 1e-5, biased variance, affine) of rows of width d <= 128,
+// one warp per row: out[r*ldo + :] = LN(in[r*ldi + :]).  nn.LayerNorm
+// (model.py:47-52,79).
+__device__ __forceinline__ void tile_layernorm(const float* in, int ldi, float* out, int ldo,
+                                               int nrows, int d,
+                                               const float* __restrict__ g,
+                                               const float* __restrict__ bta) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  for (int r = warp; r < nrows; r += nwarps) {
+    const float* x = in + r * ldi;
+    float v[4];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int c = lane + 32 * i;
+      v[i] = c < d ? x[c] : 0.f;
+      s += v[i];
+    }
+    const float mean = warp_sum(s) / float(d);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int c = lane + 32 * i;
+      float t = c < d ? v[i] - mean : 0.f;
+      q = fmaf(t, t, q);
+    }
+    const float rstd = rsqrtf(warp_sum(q) / float(d) + 1e-5f);
+    float* o = out + r * ldo;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int c = lane + 32 * i;
+      if (c < d) o[c] = (v[i] - mean) * rstd * __ldg(g + c) + __ldg(bta + c);
+    }
+  }
+}
+
+// Scatter one qkv feature (model.py:37: reshape(b, t, 3, heads, hd)) of the
+// token (b, it, s) into the spatial-attention operand layouts.
+struct QkvDst {
+  float* q; float* k; float* v;                     // precise (fp32) layouts
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;  // fast (bf16)
+  const int* rank;   // non-null: Q rows are compact (pruned consumer block)
+  int nt, ns, ns_pad, d, heads, hd;
+};
+
+__device__ __forceinline__ void qkv_store(const QkvDst& o, int b, int it, int s, int n, float v) {
+  const int which = n / o.d;
+  const int f = n - which * o.d;
+  const int hh = f / o.hd, e = f - hh * o.hd;
+  const size_t seq = size_t(b * o.nt + it) * o.heads + hh;
+  int row = s;
+  if (which == 0 && o.rank) {
+    row = o.rank[b * o.ns + s];
+    if (row < 0) return;
+  }
+  if (o.qh) {
+    if (which == 0) o.qh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
+    else if (which == 1) o.kh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
+    else o.vth[(seq * o.hd + e) * o.ns_pad + row] = __float2bfloat16_rn(v);
+  } else {
+    float* dst = which == 0 ? o.q : (which == 1 ? o.k : o.v);
+    dst[(seq * o.ns_pad + row) * o.hd + e] = v;
+  }
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {   // nn.GELU() default
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f));
+}
+
+}  // namespace nvrec
