@@ -1,0 +1,413 @@
+"""Benchmark: recovered 1280x720 RGB-D frames/s per GPU (+ p50 latency).
+
+Workload (BASELINE.json configs[2] x configs[4]): each GPU serves S
+independent 720p RGB-D conference streams (default 8, so 8 GPUs = the
+64-stream multi-party config; weak scaling, no collective on the data
+path).  One step = one frame of every stream, both modalities:
+
+  loss mask   synthetic codec P-frame headers (~10% changed blocks) whose
+              body shards are dropped by a Gilbert-Elliott channel
+              (p_gb=0.0155, p_bg=0.5, tests/test_acceptance.py:263-264)
+              -> nvrec_loss_mask (bit-exact receiver+codec mask)
+  recovery    nvrec_recover_u8 over the S streams of each modality (RGB and
+              depth on two CUDA streams): u8 stack of 5 references + the
+              corrupted plane, model forward, quantise, masked merge.
+
+``value`` = frames/s with inputs resident in HBM (device-timed, CUDA
+events, max over ranks).  ``e2e`` = the same step through host buffers:
+pinned H2D of every stream's loss-mask job and its 6 planes per modality
+(exactly what the reference recovery request carries, recovery.py:219-227)
+and D2H of the recovered planes, inside the timed region.
+
+``--impl reference`` times the reference CPU path (the oracle restatement
+of RecoveryServer._recover in fp32 torch-CPU ops -- the same ATen kernels
+the reference module calls) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W = 720, 1280
+METRIC = "recovered RGB-D frames/sec/GPU and p50 per-frame latency at 720p"
+MODS = (("rgb", 3, 1024), ("depth", 1, 512))      # name, channels, shard L
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams-per-gpu", type=int, default=8)
+    ap.add_argument("--precision", default="fast", choices=["fast", "precise"])
+    ap.add_argument("--latency-iters", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# synthetic per-rank workload
+
+class ModalityWork:
+    """S streams of one modality: references + corrupted planes, loss-mask
+    jobs, device-resident and pinned-host copies."""
+
+    def __init__(self, name, c, L, S, stream_base, device, precision):
+        from paper_2604_27441_b200 import Checkpoint, ModelConfig
+        from paper_2604_27441_b200.lossmask import LossMaskBatch, PFrameShards
+        from paper_2604_27441_b200.recovery import RecoveryEngine, stack_slots
+        from paper_2604_27441_b200.synth import GilbertElliott, p_frame_shards
+
+        self.name, self.c, self.S = name, c, S
+        cfg = ModelConfig()
+        ck = Checkpoint.random_init(cfg, c, seed=0)          # torch.manual_seed(0) init
+        self.engine = RecoveryEngine(ck.build_model(precision=precision), precision)
+        self.engine.model.native(device)
+        F = cfg.stack_len
+        rng = np.random.default_rng(1000 * c)
+        # 6 planes per stream (5 refs + corrupted plane), slot = 6*s + i
+        self.host_frames = torch.empty((S * F, H, W, c), dtype=torch.uint8).pin_memory()
+        hf = self.host_frames.numpy()
+        for s in range(S):
+            base = rng.integers(0, 256, (H // 8 + 2, W // 8 + 2, c), dtype=np.uint8)
+            tex = np.kron(base, np.ones((8, 8, 1), np.uint8))
+            for i in range(F):
+                hf[s * F + i] = tex[i % 8: i % 8 + H, 0:W]      # slow drift
+        self.frames = self.host_frames.to(device)
+        self.index = torch.tensor([[s * F + i for i in stack_slots(5, 5, F)]
+                                   for s in range(S)], dtype=torch.int32, device=device)
+        # loss-mask jobs: GE-dropped body shards of synthetic P-frame headers
+        jobs = []
+        for s in range(S):
+            ge = GilbertElliott(seed=stream_base + s + 17 * c)
+            hdr, nd, recv, enc = p_frame_shards(np.random.default_rng(stream_base + s + c),
+                                                W, H, c, L, ge.drop, present_ratio=0.1)
+            if recv.all():                     # ensure each stream needs recovery
+                recv[1 + (s % max(1, nd - 1))] = False
+            jobs.append(PFrameShards(hdr, nd, recv, L, enc))
+        self.jobs = jobs
+        nblk = (H // 16) * (W // 16)
+        self.lm = LossMaskBatch(S, max(len(j.header) for j in jobs) + 16,
+                                max(j.n_data for j in jobs) + 1, nblk, 1, device)
+        self.lm.stage(jobs)
+        self.lm.launch()
+        grids = self.lm.results()
+        self.masked_patches = [int(g.sum()) for g in grids]
+        self.out = torch.empty((S, H, W, c), dtype=torch.uint8, device=device)
+        self.host_out = torch.empty((S, H, W, c), dtype=torch.uint8).pin_memory()
+        self.plane_bytes = H * W * c
+
+    def device_step(self, stream):
+        """Loss mask + recovery with inputs resident in HBM."""
+        from paper_2604_27441_b200 import _native
+        import ctypes
+        _native.check(self.lm.lib.nvrec_loss_mask(ctypes.c_void_p(self.lm.dev_in.data_ptr()),
+                                                  self.lm.n,
+                                                  ctypes.c_void_p(int(stream.cuda_stream))))
+        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+
+    def e2e_step(self, stream):
+        """Same step through pinned host buffers (H2D in, D2H out)."""
+        self.lm.launch(stream)                               # H2D jobs + kernel
+        self.frames.copy_(self.host_frames, non_blocking=True)
+        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+        self.host_out.copy_(self.out, non_blocking=True)
+
+    def h2d_bytes(self):
+        return int(self.lm.h2d_bytes + self.host_frames.numel())
+
+    def d2h_bytes(self):
+        return int(self.host_out.numel())
+
+
+def run_steps(works, streams, fn, n):
+    main = torch.cuda.current_stream()
+    for _ in range(n):
+        ev = main.record_event()
+        for wk, st in zip(works, streams):
+            st.wait_event(ev)
+            with torch.cuda.stream(st):
+                getattr(wk, fn)(st)
+        for st in streams:
+            main.wait_stream(st)
+
+
+def timed(works, streams, fn, steps, dist_on):
+    torch.cuda.synchronize()
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    run_steps(works, streams, fn, steps)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if dist_on:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    return ms
+
+
+# ----------------------------------------------------------------------------
+# algorithmic work for the roofline of the dominant kernel
+
+def attention_flops(ns, n_masked, nt=3, heads=2, hd=32, layers=2):
+    """Spatial attention FLOPs actually required per modality-frame:
+    dense blocks need all ns queries; the last block only the masked ones
+    (exact pruning, the merge discards the rest)."""
+    per_q = 4 * ns * hd * heads * nt          # QK^T + PV per query row
+    return per_q * (ns * (layers - 1) + n_masked)
+
+
+def cpu_reference(seconds, max_frames=None):
+    """Oracle ``_recover`` restatement on host cores: 720p RGB-D frames/s."""
+    from oracle import nvrec_forward, recover as orec
+    from paper_2604_27441_b200.checkpoint import Checkpoint
+    from paper_2604_27441_b200.config import ModelConfig
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    arch = nvrec_forward.Arch()
+    rng = np.random.default_rng(3)
+    states, inputs = {}, {}
+    for name, c, _ in MODS:
+        torch.manual_seed(0)
+        ck = Checkpoint.random_init(ModelConfig(), c, seed=0)
+        states[c] = {k: v.numpy() for k, v in ck.state.items()}
+        frames = rng.integers(0, 256, (6, H, W, c), dtype=np.uint8)
+        grid = rng.random((H // 16, W // 16)) < 0.1
+        inputs[c] = (frames[-1], grid, list(frames[:-1]))
+
+    def one():
+        for _, c, _ in MODS:
+            plane, grid, refs = inputs[c]
+            orec.recover(states[c], arch, c, plane, grid, refs)
+
+    one()                                   # warm-up
+    n, t0 = 0, time.perf_counter()
+    while True:
+        one()
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (max_frames and n >= max_frames):
+            break
+    return n / el, n, el, threads
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    per = []
+    from oracle import nvrec_forward  # noqa: F401  (oracle = the reference CPU path)
+    for i in range(args.warmup + args.steps):
+        fps, n, el, threads = cpu_reference(0.0, max_frames=1)
+        if i >= args.warmup:
+            per.append(el)
+    tot = sum(per)
+    value = args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "1280x720 RGB-D recovery (configs[2]); one RGB-D frame "
+                                   "per step, 10% block mask, k=5 refs",
+                       "height": H, "width": W},
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads,
+                             "kind": "port",
+                             "sample": "%d x 720p RGB-D frames through the oracle "
+                                       "restatement of RecoveryServer._recover "
+                                       "(fp32 torch-CPU, %d threads)" % (args.steps, threads)},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    dist_on = world > 1
+    if args.impl == "reference":
+        if dist_on:
+            torch.distributed.init_process_group("gloo")
+        reference_arm(args, rank, world)
+        if dist_on:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+    from paper_2604_27441_b200 import _native
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if dist_on:
+        torch.distributed.init_process_group("nccl", device_id=device)
+    S = args.streams_per_gpu
+    works = [ModalityWork(n, c, L, S, stream_base=rank * S, device=device,
+                          precision=args.precision) for n, c, L in MODS]
+    streams = [torch.cuda.Stream(device) for _ in works]
+
+    # warm-up (both paths), then the device-resident timed region
+    run_steps(works, streams, "device_step", args.warmup)
+    run_steps(works, streams, "e2e_step", max(1, args.warmup // 2))
+    clocks = ClockSampler(local)
+    ms = timed(works, streams, "device_step", args.steps, dist_on)
+    clk = clocks.stop()
+    # end-to-end through host buffers
+    ms_e2e = timed(works, streams, "e2e_step", args.steps, dist_on)
+    # per-stage device times (separate pass with event brackets)
+    torch.cuda.synchronize()
+    with _native.StageProfile() as prof:
+        run_steps(works, streams, "device_step", args.steps)
+        torch.cuda.synchronize()
+
+    # single-stream RGB-D latency (b = 1 per modality, e2e through host buffers)
+    lat = []
+    if rank == 0:
+        single = [ModalityWork(n, c, L, 1, stream_base=999, device=device,
+                               precision=args.precision) for n, c, L in MODS]
+        sst = [torch.cuda.Stream(device) for _ in single]
+        run_steps(single, sst, "e2e_step", 5)
+        for _ in range(args.latency_iters):
+            lat.append(timed(single, sst, "e2e_step", 1, False))
+        lat_dev = [timed(single, sst, "device_step", 1, False)
+                   for _ in range(args.latency_iters)]
+
+    if dist_on:
+        torch.distributed.barrier()
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+
+    frames = S * world * args.steps
+    value = frames / (ms / 1000.0)
+    e2e = frames / (ms_e2e / 1000.0)
+    # roofline of the dominant kernel (spatial attention)
+    ns = (H // 16) * (W // 16)
+    att_kind = "attn_tc" if prof.launches["attn_tc"] else "attn_simt"
+    att_ms = prof.ms[att_kind]
+    att_launches = prof.launches[att_kind]
+    flops = 0
+    for wk in works:
+        for m in wk.masked_patches:
+            flops += attention_flops(ns, m)
+    flops *= args.steps
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peaks = json.load(open(peaks_path))
+        peak, peak_src = peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (burst)"
+    else:
+        peak, peak_src = 1590.0, "fallback B200_PROFILING.md"
+    achieved = flops / (att_ms / 1000.0) / 1e12 if att_ms else 0.0
+    step_ms_prof = sum(prof.ms.values()) / args.steps
+    launches_per_step = prof.total_launches / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if (args.precision == "fast" and prof.launches["attn_tc"]) else "f32",
+        "data": "synthetic",
+        "config": {"workload": "1280x720 RGB-D streams (configs[2] x configs[4]): %d "
+                               "streams/GPU, GE loss (p_gb=0.0155,p_bg=0.5) on body shards of "
+                               "synthetic P-frame headers, k=5 refs" % S,
+                   "streams_per_gpu": S, "height": H, "width": W,
+                   "precision": args.precision,
+                   "masked_patches_per_frame": {wk.name: float(np.mean(wk.masked_patches))
+                                                for wk in works},
+                   "l2": "inputs larger than L2 (%.0f MB of u8 planes per step > 126 MB)"
+                         % (sum(wk.host_frames.numel() for wk in works) / 1e6)},
+        "clocks": clk,
+        "e2e": {"value": e2e, "unit": "frames/s",
+                "h2d_bytes_per_step": sum(wk.h2d_bytes() for wk in works),
+                "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works)},
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "p50_latency_ms": statistics.median(lat),
+        "p99_latency_ms": float(np.percentile(lat, 99)),
+        "p50_latency_device_ms": statistics.median(lat_dev),
+        "latency_note": "single stream, one RGB-D frame (both modalities on two CUDA "
+                        "streams), e2e through pinned host buffers incl. H2D of 6 planes "
+                        "per modality and D2H of the result",
+        "stage_ms_per_step": {k: v / args.steps for k, v in prof.ms.items() if v},
+        "roofline": {"kernel": att_kind, "bound": "tensor", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "share_of_step": att_ms / max(1e-9, sum(prof.ms.values())),
+                     "algorithmic_flops_per_launch": flops / max(1, att_launches)},
+    }
+    if not args.no_cpu_baseline:
+        fps, n, el, threads = cpu_reference(args.cpu_seconds)
+        line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": threads,
+                                "kind": "port",
+                                "sample": "%d x 720p RGB-D frames (%.1f s) through the oracle "
+                                          "restatement of RecoveryServer._recover, fp32 "
+                                          "torch-CPU, %d threads" % (n, el, threads)}
+    print(json.dumps(line), flush=True)
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

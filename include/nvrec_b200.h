@@ -126,6 +126,18 @@ typedef struct nvrec_lossmask_job {
  * Bit-exact with the reference receiver+codec. */
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream);
 
+/* Optional per-stage timing for benchmarks: between begin and end every
+ * kernel launch is bracketed by CUDA events on its stream; end synchronises
+ * and returns the summed milliseconds and launch counts per NVREC_STAGE_*.
+ * Returns the number of timed launches.  Not thread-safe; off by default. */
+enum {
+  NVREC_STAGE_LOSSMASK = 0, NVREC_STAGE_MASKLIST = 1, NVREC_STAGE_COPY = 2,
+  NVREC_STAGE_EMBED = 3, NVREC_STAGE_LNQKV = 4, NVREC_STAGE_ATTN_SIMT = 5,
+  NVREC_STAGE_ATTN_TC = 6, NVREC_STAGE_TOKEN = 7, NVREC_NUM_STAGES = 8
+};
+int nvrec_profile_begin(void);
+int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages);
+
 #ifdef __cplusplus
 }
 #endif

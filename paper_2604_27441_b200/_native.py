@@ -26,7 +26,10 @@ E_INVALID, E_UNSUPPORTED, E_CUDA, E_WORKSPACE, E_STATE = -1, -2, -3, -4, -5
 
 EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_model_destroy", "nvrec_model_load", "nvrec_workspace_bytes",
-           "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask")
+           "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask",
+           "nvrec_profile_begin", "nvrec_profile_end")
+STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
+          "token")
 
 
 class NativeError(RuntimeError):
@@ -81,6 +84,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_recover_u8.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                          i64, i32, vp]
         lib.nvrec_loss_mask.argtypes = [vp, i32, vp]
+        lib.nvrec_profile_end.argtypes = [ctypes.POINTER(ctypes.c_float),
+                                          ctypes.POINTER(i32), i32]
         for name in EXPORTS:
             getattr(lib, name)
         if lib.nvrec_abi_version() != 1:
@@ -180,3 +185,24 @@ class NativeModel:
                                         out.data_ptr(), ws.data_ptr(), ws.numel(), prec,
                                         stream_ptr()))
         return out
+
+
+class StageProfile:
+    """Context manager around ``nvrec_profile_begin/end``: per-stage device
+    milliseconds and launch counts of every library kernel launched inside."""
+
+    def __enter__(self):
+        check(load_library().nvrec_profile_begin())
+        return self
+
+    def __exit__(self, *exc):
+        n = len(STAGES)
+        ms = (ctypes.c_float * n)()
+        cnt = (ctypes.c_int32 * n)()
+        total = load_library().nvrec_profile_end(ms, cnt, n)
+        if total < 0:
+            check(total)
+        self.ms = {STAGES[i]: float(ms[i]) for i in range(n)}
+        self.launches = {STAGES[i]: int(cnt[i]) for i in range(n)}
+        self.total_launches = int(total)
+        return False

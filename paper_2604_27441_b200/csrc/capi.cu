@@ -36,6 +36,31 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 }  // namespace
 
+
+// ---- optional per-stage timing (bench.py roofline) ----------------------------
+// When enabled, every kernel launch of the library is bracketed by a pair of
+// CUDA events recorded on the launching stream; nvrec_profile_end sums the
+// durations per stage.  Off by default (zero overhead on the hot path).
+namespace {
+constexpr int kProfMax = 8192;
+struct ProfRec { cudaEvent_t a, b; int kind; };
+bool g_prof = false;
+std::vector<ProfRec> g_prof_pool;
+int g_prof_n = 0;
+
+struct ProfScope {
+  ProfRec* r = nullptr;
+  cudaStream_t s;
+  ProfScope(int kind, cudaStream_t st) : s(st) {
+    if (!g_prof || g_prof_n >= int(g_prof_pool.size())) return;
+    r = &g_prof_pool[g_prof_n++];
+    r->kind = kind;
+    cudaEventRecord(r->a, s);
+  }
+  ~ProfScope() { if (r) cudaEventRecord(r->b, s); }
+};
+}  // namespace
+
 struct nvrec_model {
   nvrec_config cfg;
   nvrec::Dims D;
@@ -171,6 +196,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     // block li's spatial attention: Q/K/V were written by the previous stage
     cudaError_t e;
     if (fast) {
+      ProfScope ps(NVREC_STAGE_ATTN_TC, s);
       e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s);
     } else {
       nvrec::AttnArgs aa{};
@@ -178,6 +204,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
       aa.count = prune_here ? A.count : nullptr;
       aa.nt = D.nt; aa.heads = D.heads; aa.ns = A.ns; aa.ns_pad = A.ns_pad; aa.d = D.d;
       aa.scale_log2 = 1.4426950408889634f / sqrtf(float(D.hd));
+      ProfScope ps(NVREC_STAGE_ATTN_SIMT, s);
       e = nvrec::launch_attn_simt(aa, b, A.ns, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "spatial attention launch");
@@ -196,7 +223,10 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     ta.dst.rank = (!last && li + 1 == D.layers - 1 && pruned) ? A.rank : nullptr;
     ta.img_h = h; ta.img_w = w; ta.nh = A.nh; ta.nw = A.nw; ta.ns = A.ns;
     ta.out_f32 = out_f32; ta.out_u8 = out_u8;
-    e = nvrec::launch_token(ta, b, A.ns, s);
+    {
+      ProfScope ps(NVREC_STAGE_TOKEN, s);
+      e = nvrec::launch_token(ta, b, A.ns, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "token kernel launch");
   }
   return 0;
@@ -388,7 +418,11 @@ static int embed_and_qkv0(const nvrec_model* m, nvrec::Act& A, bool u8, const fl
   ea.stack = stack; ea.f_in = f; ea.pmask = pmask;
   ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns;
   ea.x = A.x;
-  cudaError_t e = nvrec::launch_embed(ea, u8, A.b, s);
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_EMBED, s);
+    e = nvrec::launch_embed(ea, u8, A.b, s);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "embed launch");
   nvrec::LnQkvArgs la{};
   la.D = D;
@@ -401,7 +435,10 @@ static int embed_and_qkv0(const nvrec_model* m, nvrec::Act& A, bool u8, const fl
   la.dst.nt = D.nt; la.dst.ns = A.ns; la.dst.ns_pad = A.ns_pad; la.dst.d = D.d;
   la.dst.heads = D.heads; la.dst.hd = D.hd;
   la.ns = A.ns;
-  e = nvrec::launch_ln_qkv(la, A.b, s);
+  {
+    ProfScope ps(NVREC_STAGE_LNQKV, s);
+    e = nvrec::launch_ln_qkv(la, A.b, s);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "ln_qkv launch");
   return 0;
 }
@@ -439,9 +476,16 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   nvrec::Act A = make_act(m, ws, L, b, h, w);
   const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
   const int nbytes = (A.ns + 7) / 8;
-  cudaError_t e = nvrec::launch_masklist(mask_bits, b, nbytes, A.ns, A.list, A.rank, A.count, s);
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_MASKLIST, s);
+    e = nvrec::launch_masklist(mask_bits, b, nbytes, A.ns, A.list, A.rank, A.count, s);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "masklist launch");
-  e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
+  {
+    ProfScope ps(NVREC_STAGE_COPY, s);
+    e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "copy launch");
   rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
   if (rc) return rc;
@@ -450,9 +494,45 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
 
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream) {
   if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(NVREC_E_INVALID, "bad job array");
-  cudaError_t e = nvrec::launch_lossmask(jobs, n_jobs, static_cast<cudaStream_t>(stream));
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_LOSSMASK, static_cast<cudaStream_t>(stream));
+    e = nvrec::launch_lossmask(jobs, n_jobs, static_cast<cudaStream_t>(stream));
+  }
   if (e != cudaSuccess) return cuda_fail(e, "loss-mask launch");
   return 0;
+}
+
+
+int nvrec_profile_begin(void) {
+  if (g_prof_pool.empty()) {
+    g_prof_pool.resize(kProfMax);
+    for (auto& r : g_prof_pool) {
+      CK(cudaEventCreate(&r.a), "cudaEventCreate");
+      CK(cudaEventCreate(&r.b), "cudaEventCreate");
+    }
+  }
+  g_prof_n = 0;
+  g_prof = true;
+  return 0;
+}
+
+int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages) {
+  g_prof = false;
+  for (int i = 0; i < n_stages; ++i) { ms_per_stage[i] = 0.f; launches_per_stage[i] = 0; }
+  for (int i = 0; i < g_prof_n; ++i) {
+    ProfRec& r = g_prof_pool[i];
+    CK(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+    if (r.kind >= 0 && r.kind < n_stages) {
+      ms_per_stage[r.kind] += ms;
+      launches_per_stage[r.kind] += 1;
+    }
+  }
+  int n = g_prof_n;
+  g_prof_n = 0;
+  return n;
 }
 
 }  // extern "C"
