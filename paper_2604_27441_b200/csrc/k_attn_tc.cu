@@ -1,13 +1,324 @@
-// k_attn_tc.cu -- tcgen05/TMEM spatial attention (bf16 operands, fp32
-// softmax/accumulation) for head_dim 32.  (placeholder: not yet enabled)
+// k_attn_tc.cu -- tcgen05/TMEM flash attention for the spatial attention of
+// the nvrec blocks (F.scaled_dot_product_attention at model.py:39, called on
+// (b*nt, ns, d) at model.py:59-60): softmax(Q K^T / sqrt(32)) V per (stream,
+// time slice, head), non-causal, unmasked, head_dim 32, bf16 operands, fp32
+// scores / softmax / output.
+//
+// CTA = two 128-query tiles (ping-pong) of one (slice, head) sequence;
+// 10 warps:
+//   warps 0-3  softmax of query tile 0    (TMEM lanes 0-127, one row/thread)
+//   warps 4-7  softmax of query tile 1
+//   warp  8    TMA producer: Q tiles once, then K/V tiles through a 3-stage
+//              ring (K: 128 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x 2 x 128 B,
+//              SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
+//   warp  9    MMA issuer (one thread): S_t = Q_t K^T (M128 N128 K32, fp32 in
+//              TMEM), then PV_t = P_t V (M128 N32 K128, P read from TMEM where
+//              the softmax warps stored it as packed bf16 over S_t)
+// TMEM (512 columns): tile t owns S at [256t, 256t+128) and PV at
+// [256t+128, 256t+160).  Per key tile j a softmax thread loads its S row
+// (128 fp32), folds the previous PV into its register-resident output with
+// the previous rescale factor, computes the online-softmax probabilities in
+// base 2, and stores P (bf16) back into TMEM.  MMAs of one thread execute in
+// issue order, so "S_t(j+1) after PV_tj" needs no extra fence, and the
+// commit after S_t(j+1) also certifies PV_tj.
+//
+// The score rescale is the dominant cost: 128 MUFU ex2 per row per key tile
+// (the path is exp-bound).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "launch.cuh"
+#include "sm100.cuh"
 
 namespace nvrec {
 
-bool tc_supported(const Dims& D) { return false; }
+namespace {
+
+using namespace sm100;
+
+constexpr int kHd = 32;
+constexpr int kTileQ = 128;
+constexpr int kTileK = 128;
+constexpr int kStages = 3;
+constexpr int kThreads = 320;
+constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
+constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
+constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
+constexpr uint32_t kIdescS = idesc_bf16(128, 128);
+constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
+
+struct __align__(1024) Smem {
+  uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
+  uint8_t q[2][kQBytes];            // 512-aligned (SWIZZLE_64B atoms)
+  uint8_t k[kStages][kKBytes];
+  uint64_t q_full;
+  uint64_t kv_full[kStages], kv_empty[kStages];
+  uint64_t s_full[2], p_full[2];
+  uint32_t tmem_base;
+};
+
+struct TcArgs {
+  float* ao;          // [b][nt][ns][64]
+  const int* count;   // compact query count per stream, or null (= ns)
+  int nt, heads, ns, d;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+               const __grid_constant__ CUtensorMap tm_k,
+               const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seq = blockIdx.y;
+  const int b = seq / (a.nt * a.heads);
+  const int nq = a.count ? a.count[b] : a.ns;
+  const int q0 = blockIdx.x * 2 * kTileQ;
+  if (q0 >= nq) return;                                   // uniform across the CTA
+  const int nkv = (a.ns + kTileK - 1) / kTileK;
+
+  if (warp == 8 && lane == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+  }
+  if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(&sm.q_full, 2 * kQBytes);
+      tma_load_3d(sm.q[0], &tm_q, &sm.q_full, 0, q0, seq);
+      tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, q0 + kTileQ, seq);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kStages;
+        mbar_wait(&sm.kv_empty[s], ((j / kStages) & 1) ^ 1);
+        mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
+        tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, j * kTileK, seq);
+        tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], j * kTileK, 0, seq);
+        tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint64_t qdesc[2][2];
+      for (int t = 0; t < 2; ++t)
+        for (int kk = 0; kk < 2; ++kk)
+          qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
+      auto issue_s = [&](int t, int s) {
+        const uint32_t kb = smem_u32(sm.k[s]);
+        for (int kk = 0; kk < 2; ++kk)
+          mma_ss(tmem + 256 * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
+                 kIdescS, kk);
+        mma_commit(&sm.s_full[t]);
+      };
+      mbar_wait(&sm.q_full, 0);
+      mbar_wait(&sm.kv_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kStages;
+        const bool more = j + 1 < nkv;
+        const int s1 = (j + 1) % kStages;
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&sm.p_full[t], j & 1);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sm.v[s]);
+          for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
+            const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+            mma_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8,
+                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+          }
+          if (t == 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
+          if (more) {
+            if (t == 0) {
+              mbar_wait(&sm.kv_full[s1], ((j + 1) / kStages) & 1);
+              tc_fence_after();
+            }
+            issue_s(t, s1);
+          } else {
+            mma_commit(&sm.s_full[t]);               // final: PV_t(last) done
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int t = warp >> 2;                 // query tile
+    const int quarter = warp & 3;            // TMEM lane quarter
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + 256 * t;
+    const uint32_t t_pv = t_s + 128;
+    float o[kHd];
+#pragma unroll
+    for (int e = 0; e < kHd; ++e) o[e] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&sm.s_full[t], j & 1);
+      tc_fence_after();
+      const int valid = a.ns - j * kTileK;   // keys of this tile that exist
+      // pass 1: row max of the raw scores (32-column chunks keep registers low)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(t_s + 32 * ch, r);
+        tmem_wait_ld();
+        if (valid >= kTileK) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(r[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            mx = fmaxf(mx, 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+        }
+      }
+      // fold the previous tile's P V into the register-resident output
+      if (j > 0) {
+        uint32_t pv[32];
+        tmem_ld32(t_pv, pv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < kHd; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(pv[e]));
+      }
+      const float mn = fmaxf(m, mx * a.scale_log2);
+      const float alpha = ex2(m - mn);
+      // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
+      // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
+      // P pairs to columns [16ch, 16ch+16))
+      float sum = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32], pk[16];
+        tmem_ld32(t_s + 32 * ch, r);
+        tmem_wait_ld();
+        if (valid < kTileK) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(r[c]), a.scale_log2, -mn));
+          const float p1 = ex2(fmaf(__uint_as_float(r[c + 1]), a.scale_log2, -mn));
+          sum += p0 + p1;
+          pk[c >> 1] = pack_bf16(p0, p1);
+        }
+        tmem_st16(t_s + 16 * ch, pk);
+      }
+      l = l * alpha + sum;
+      m = mn;
+      alpha_prev = alpha;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full[t]);
+    }
+    mbar_wait(&sm.s_full[t], nkv & 1);
+    tc_fence_after();
+    {
+      uint32_t pv[32];
+      tmem_ld32(t_pv, pv);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < kHd; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(pv[e]));
+    }
+    const int q = q0 + t * kTileQ + row;
+    if (q < nq) {
+      const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
+      const float inv = 1.f / l;
+      float4* dst = reinterpret_cast<float4*>(
+          a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
+#pragma unroll
+      for (int e = 0; e < kHd; e += 4)
+        dst[e / 4] = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// ---- host: tensor maps ---------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1,
+                 CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s) {
-  return cudaErrorNotSupported;
+  const int seqs = A.b * D.nt * D.heads;
+  CUtensorMap tq, tk, tv;
+  const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
+  // Q/K: [seq][ns_pad][32] bf16 viewed (32, ns, seq); rows >= ns read as zero
+  if (!make_map_3d(&tq, A.qh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileQ,
+                   CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map_3d(&tk, A.kh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileK,
+                   CU_TENSOR_MAP_SWIZZLE_64B) ||
+      // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 64-key boxes (128 B rows)
+      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 64, kHd,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  TcArgs ta;
+  ta.ao = A.ao;
+  ta.count = count;
+  ta.nt = D.nt;
+  ta.heads = D.heads;
+  ta.ns = A.ns;
+  ta.d = D.d;
+  ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
+  const size_t smem = sizeof(Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  dim3 grid(ceil_div(A.ns, 2 * kTileQ), seqs);
+  attn_tc_kernel<<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  return cudaGetLastError();
 }
 
 }  // namespace nvrec
