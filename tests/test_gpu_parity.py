@@ -166,3 +166,43 @@ def test_masked_pixels_do_not_leak_and_deterministic():
     s = torch.rand(1, 6, 3, 32, 32).cuda()
     mk = torch.rand(1, 32, 32).cuda() < 0.3
     assert torch.equal(m64(s, mk), m64(s, mk))
+
+
+def test_fast_path_runs_tensor_core_attention():
+    """The fast path must launch the tcgen05 attention kernel (no silent
+    fall-back to the CUDA-core kernel) and the precise path the fp32 one."""
+    from paper_2604_27441_b200 import _native
+    p = _pkg()
+    m = p.MaskedVideoModel(p.ModelConfig(), 3)
+    s = torch.rand(1, 6, 3, 64, 64).cuda()
+    mk = torch.rand(1, 64, 64).cuda() < 0.3
+    with _native.StageProfile() as prof:
+        m(s, mk)
+        torch.cuda.synchronize()
+    assert prof.launches["attn_tc"] == 2 and prof.launches["attn_simt"] == 0
+    m.precision = "precise"
+    with _native.StageProfile() as prof:
+        m(s, mk)
+        torch.cuda.synchronize()
+    assert prof.launches["attn_simt"] == 2 and prof.launches["attn_tc"] == 0
+
+
+def test_fast_vs_reference_error_budget_720p():
+    """bf16 tensor-core attention error at 1280x720 stays well inside 1e-2."""
+    arch = nvrec_forward.Arch()
+    rng = np.random.default_rng(11)
+    for c in (3, 1):
+        state = make_state(arch, c, 1100 + c)
+        stack = rng.random((1, 6, c, 720, 1280), dtype=np.float32)
+        mask = np.repeat(np.repeat(block_grid(rng, 45, 80, 0.1), 16, 0), 16, 1)[None]
+        want = nvrec_forward.forward(state, arch, c, stack, mask).numpy()
+        got = _model(arch, c, state, "fast")(torch.from_numpy(stack).cuda(),
+                                            torch.from_numpy(mask).cuda()).cpu().numpy()
+        err = np.abs(got - want)
+        print("c=%d fast max-abs %.2e mean %.2e" % (c, err.max(), err.mean()))
+        assert err.max() <= 1e-2
+        got = _model(arch, c, state, "precise")(torch.from_numpy(stack).cuda(),
+                                               torch.from_numpy(mask).cuda()).cpu().numpy()
+        err = np.abs(got - want)
+        print("c=%d precise max-abs %.2e (x65535 = %.3f)" % (c, err.max(), err.max() * 65535))
+        assert err.max() * 65535 <= 1.0
