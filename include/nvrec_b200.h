@@ -92,14 +92,14 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b,
                       int64_t workspace_bytes, int32_t precision, void* stream);
 
 /* RecoveryServer._recover over a batch of independent streams (block mask).
- * frames: u8 planes (h, w, c) packed at `frames + slot * h*w*c`;
- * frame_index: int32 (b, stack_len) slot of each stacked frame, oldest first,
+ * frames: n_slots u8 planes (h, w, c) packed at `frames + slot * h*w*c`;
+ * frame_index: int32 (b, stack_len) slot (< n_slots) of each stacked frame, oldest first,
  *   already front-padded, the last entry the corrupted plane;
  * mask_bits: u8 (b, ceil(gh*gw/8)) wire bitset (MSB-first, row-major);
  * out: u8 (b, h, w, c) merged planes (unmasked pixels = corrupted plane).
  * Only masked patches are decoded (exact: the merge discards the rest). */
 int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
-                     const uint8_t* frames, const int32_t* frame_index,
+                     const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
                      const uint8_t* mask_bits, uint8_t* out, void* workspace,
                      int64_t workspace_bytes, int32_t precision, void* stream);
 

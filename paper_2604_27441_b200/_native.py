@@ -81,7 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_workspace_bytes.restype = i64
         lib.nvrec_forward_f32.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp,
                                           vp, i64, i32, vp]
-        lib.nvrec_recover_u8.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp,
+        lib.nvrec_recover_u8.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp, vp,
                                          i64, i32, vp]
         lib.nvrec_loss_mask.argtypes = [vp, i32, vp]
         lib.nvrec_profile_end.argtypes = [ctypes.POINTER(ctypes.c_float),
@@ -181,7 +181,7 @@ class NativeModel:
                    prec: int) -> torch.Tensor:
         ws = self.workspace(b, h, w, prec)
         check(self.lib.nvrec_recover_u8(self.handle, b, h, w, frames.data_ptr(),
-                                        frame_index.data_ptr(), mask_bits.data_ptr(),
+                                        frames.shape[0], frame_index.data_ptr(), mask_bits.data_ptr(),
                                         out.data_ptr(), ws.data_ptr(), ws.numel(), prec,
                                         stream_ptr()))
         return out

@@ -67,6 +67,7 @@ struct nvrec_model {
   int device = 0;
   float* blob = nullptr;        // all packed fp32 weights
   size_t blob_floats = 0;
+  __half* blob_bf16 = nullptr;          // tensor-core operand packs (fast path, fp16)
   nvrec::ModelW W{};
   bool loaded = false;
 };
@@ -254,6 +255,7 @@ int nvrec_model_create(const nvrec_config* cfg, int32_t channels, nvrec_model** 
 int nvrec_model_destroy(nvrec_model* m) {
   if (!m) return 0;
   if (m->blob) cudaFree(m->blob);
+  if (m->blob_bf16) cudaFree(m->blob_bf16);
   delete m;
   return 0;
 }
@@ -355,6 +357,39 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
   m->W.norm_b = B + off[6];
   m->W.head_w = B + off[7];
   m->W.head_b = B + off[8];
+  // ---- bf16 UMMA packs for the tensor-core path ----------------------------
+  if (m->blob_bf16) { cudaFree(m->blob_bf16); m->blob_bf16 = nullptr; }
+  if (nvrec::embed_tc_supported(D)) {
+    // fp16 operands: u8 pixels are exact in fp16 and fp16 keeps 3 more
+    // mantissa bits of the weights than bf16
+    std::vector<__half> hb;
+    auto pack = [&](int N, int K, auto at) {   // at(n, k) -> float
+      size_t base = hb.size();
+      hb.resize(base + size_t(N) * K);
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < K; ++k)
+          hb[base + (size_t(k / 8) * (N / 8) + n / 8) * 64 + (n % 8) * 8 + k % 8] =
+              __float2half_rn(at(n, k));
+      return base;
+    };
+    const int kst = 32 * c;                         // K per stage: 2 patch rows
+    std::vector<size_t> stage_off;
+    for (int st = 0; st < T * 8; ++st) {
+      const int tt = st / 8, py0 = 2 * (st % 8);
+      stage_off.push_back(pack(d, kst, [&](int n, int k) {
+        const int pyl = k / (16 * c), rem = k % (16 * c), px = rem / c, ci = rem % c;
+        return ew_at(n, ci, tt, py0 + pyl, px);
+      }));
+    }
+    const float* q0 = t[3 + 2];                      // blocks.0.attn_s.qkv.weight (3d, d)
+    size_t qoff = pack(3 * d, d, [&](int n, int k) { return q0[size_t(n) * d + k]; });
+    CK(cudaMalloc(&m->blob_bf16, hb.size() * sizeof(__half)), "cudaMalloc(fp16)");
+    CK(cudaMemcpy(m->blob_bf16, hb.data(), hb.size() * sizeof(__half),
+                  cudaMemcpyHostToDevice), "cudaMemcpy(fp16)");
+    m->W.tc.emb = m->blob_bf16 + stage_off[0];
+    m->W.tc.emb_stage_elems = d * kst;
+    m->W.tc.qkv0 = m->blob_bf16 + qoff;
+  }
   m->loaded = true;
   return 0;
 }
@@ -462,7 +497,7 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b, int32
 }
 
 int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
-                     const uint8_t* frames, const int32_t* frame_index,
+                     const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
                      const uint8_t* mask_bits, uint8_t* out, void* ws, int64_t ws_bytes,
                      int32_t precision, void* stream) {
   WorkspaceLayout L;
@@ -472,6 +507,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     return fail(NVREC_E_UNSUPPORTED, "u8 recover path needs patch == mask block (16)");
   if (!frames || !frame_index || !mask_bits || !out)
     return fail(NVREC_E_INVALID, "null pointer");
+  if (n_slots < 1) return fail(NVREC_E_INVALID, "n_slots must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   nvrec::Act A = make_act(m, ws, L, b, h, w);
   const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
@@ -487,8 +523,28 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "copy launch");
-  rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
-  if (rc) return rc;
+  if (fast && nvrec::embed_tc_supported(m->D)) {
+    nvrec::EmbedTcArgs ea{};
+    ea.D = m->D;
+    ea.tcw = &m->W.tc;
+    ea.emb_wmsum = m->W.emb_wmsum; ea.emb_b = m->W.emb_b; ea.time_pos = m->W.time_pos;
+    ea.ln_w = m->W.blk[0].ln_s_w; ea.ln_b = m->W.blk[0].ln_s_b; ea.qkv_b = m->W.blk[0].qkv_s_b;
+    ea.frames = frames; ea.frame_index = frame_index;
+    ea.n_slots = n_slots;
+    ea.rank = A.rank;
+    ea.qrank = m->D.layers == 1 ? A.rank : nullptr;
+    ea.x = A.x; ea.qh = A.qh; ea.kh = A.kh; ea.vth = A.vth;
+    ea.b = b; ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns; ea.ns_pad = A.ns_pad;
+    cudaError_t e2;
+    {
+      ProfScope ps(NVREC_STAGE_EMBED, s);
+      e2 = nvrec::launch_embed_tc(ea, s);
+    }
+    if (e2 != cudaSuccess) return cuda_fail(e2, "embed_tc launch");
+  } else {
+    rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
+    if (rc) return rc;
+  }
   return run_blocks(m, A, L, fast, true, h, w, nullptr, out, s);
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "nvrec_b200.h"
@@ -36,7 +37,17 @@ struct BlockW {
   const float *ln_m_w, *ln_m_b, *fc1_w, *fc1_b, *fc2_w, *fc2_b;
 };
 
+// fp16 operands of the tensor-core (fast) path, pre-packed in the UMMA
+// no-swizzle K-major "interleaved" layout: element (n, k) of an N x K block at
+// ((k/8)*(N/8) + n/8)*64 + (n%8)*8 + k%8 (core matrices of 8 rows x 16 B).
+struct TcW {
+  const __half* emb;            // [T*8 stages][64 x 32c] embed weight blocks
+  const __half* qkv0;           // [192 x 64] block-0 qkv_s weight
+  int emb_stage_elems;          // 64 * 32c
+};
+
 struct ModelW {
+  TcW tc;
   const float* emb_w;      // [kimg][d], k = ((tt*p+py)*p+px)*c+ci
   const float* emb_wmask;  // [p*p][d] mask-channel weights at tt = T-1
   const float* emb_wmsum;  // [d]      sum of emb_wmask over pixels

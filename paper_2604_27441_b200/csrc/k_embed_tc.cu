@@ -1,0 +1,314 @@
+// k_embed_tc.cu -- tcgen05 implicit-GEMM tubelet embedding (the "encoder
+// convolution", model.py:73-74,111) fused with its epilogue (x/255 scale,
+// bias, time_pos, mask-channel rank-1 term, model.py:102-114) and with block
+// 0's LN_s + qkv_s projection (model.py:59 -> :37), for the u8 server path.
+//
+// CTA = 128 tokens = an 8 x 16 rectangle of patches of one (stream, time
+// slice); 6 warps:
+//   warp 4     producer: per K stage (tubelet frame tt, 2 patch rows) one 5-D
+//              TMA box of raw u8 pixels [8 ih][2 py][16 iw][16*c bytes]
+//              straight from the HWC planes (zero-filled past the frame edge)
+//              and one bulk copy of the stage's fp16 weight block
+//   warps 0-3  converters: u8 -> fp16 (exact: byte_perm into 1024+v, then
+//              -1024) written as the UMMA A operand (no-swizzle K-major core
+//              matrices); masked patches of the corrupted frame become zeros
+//   warp 5     MMA: D[128 x 64] += A[128 x 32c] W^T per stage (fp32 in TMEM),
+//              then the qkv GEMM [128 x 64] x [64 x 192] on the LN output
+//   warps 0-3  epilogue: TMEM -> registers (one token row per thread),
+//              x = acc/255 + bias + time_pos (+ sum of mask-channel weights),
+//              store x (fp32), LayerNorm in registers -> fp16 A2, then
+//              q/k/v + bias -> bf16 attention operands (Q, K rows; V^T).
+// GEMM per token: K = 512c (c = 3: 1536), N = 64; the u8 planes are read
+// once from HBM by TMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "launch.cuh"
+#include "sm100.cuh"
+
+namespace nvrec {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kRows = 128;
+constexpr int kTh = 8, kTw = 16;   // patch rectangle per CTA
+constexpr int kNst = 3;            // pipeline depth
+constexpr int kThreads = 192;
+
+template <int C>
+struct __align__(128) EmbSmem {
+  static constexpr uint32_t kU8 = kTh * 2 * kTw * 16 * C;   // raw pixels per stage
+  static constexpr uint32_t kA = kRows * 32 * C * 2;        // fp16 A per stage
+  static constexpr uint32_t kW = 64 * 32 * C * 2;           // fp16 W per stage
+  uint8_t a[kNst][kA];
+  uint8_t w[kNst][kW];
+  uint8_t u8[kNst][kU8];
+  uint8_t a2[kRows * 64 * 2];
+  uint8_t wq[192 * 64 * 2];
+  uint64_t full[kNst], aready[kNst], empty[kNst];
+  uint64_t acc_full, wq_full, a2_ready, qkv_full;
+  uint32_t tmem_base;
+  int slot[16];
+};
+
+__device__ __forceinline__ uint32_t u8x2_to_h2(uint32_t w, uint32_t sel) {
+  uint32_t p = __byte_perm(w, 0x64646464u, sel);     // fp16 1024 + byte
+  __half2 h = *reinterpret_cast<__half2*>(&p);
+  h = __hsub2(h, __half2half2(__ushort_as_half(0x6400)));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int C>
+__global__ void __launch_bounds__(kThreads, 1)
+embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tcw) {
+  extern __shared__ uint8_t smem_raw[];
+  using S = EmbSmem<C>;
+  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_w = (a.nw + kTw - 1) / kTw;
+  const int ih0 = (blockIdx.x / tiles_w) * kTh, iw0 = (blockIdx.x % tiles_w) * kTw;
+  const int it = blockIdx.y, b = blockIdx.z;
+  const int T = a.D.T, nst = T * 8;
+
+  if (warp == 4 && lane == 0) {
+    for (int i = 0; i < kNst; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.aready[i], 128);
+      mbar_init(&sm.empty[i], 1);
+    }
+    mbar_init(&sm.acc_full, 1);
+    mbar_init(&sm.wq_full, 1);
+    mbar_init(&sm.a2_ready, 128);
+    mbar_init(&sm.qkv_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&tm_u8);
+  }
+  if (threadIdx.x < T) sm.slot[threadIdx.x] = a.frame_index[b * a.D.F + it * T + threadIdx.x];
+  if (warp == 0) tmem_alloc<256>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 4) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      mbar_expect_tx(&sm.wq_full, 192 * 64 * 2);
+      bulk_load(sm.wq, tcw.qkv0, 192 * 64 * 2, &sm.wq_full);
+      for (int st = 0; st < nst; ++st) {
+        const int ps = st % kNst;
+        mbar_wait(&sm.empty[ps], ((st / kNst) & 1) ^ 1);
+        mbar_expect_tx(&sm.full[ps], S::kU8 + S::kW);
+        tma_load_5d(sm.u8[ps], &tm_u8, &sm.full[ps], 0, iw0, 2 * (st % 8), ih0,
+                    sm.slot[st / 8]);
+        bulk_load(sm.w[ps], tcw.emb + size_t(st) * tcw.emb_stage_elems, S::kW, &sm.full[ps]);
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------------------------------------------------------- MMA
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16(128, 64);
+      for (int st = 0; st < nst; ++st) {
+        const int ps = st % kNst;
+        mbar_wait(&sm.aready[ps], (st / kNst) & 1);
+        tc_fence_after();
+        const uint32_t ab = smem_u32(sm.a[ps]), wb = smem_u32(sm.w[ps]);
+#pragma unroll
+        for (int kk = 0; kk < 2 * C; ++kk)
+          mma_ss(tmem, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
+                 sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
+        mma_commit(&sm.empty[ps]);
+      }
+      mma_commit(&sm.acc_full);
+      mbar_wait(&sm.wq_full, 0);
+      mbar_wait(&sm.a2_ready, 0);
+      tc_fence_after();
+      const uint32_t idesc2 = idesc_f16(128, 192);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_ss(tmem + 64, sdesc(smem_u32(sm.a2) + kk * 4096, 128, kSwizzleNone, 2048),
+               sdesc(smem_u32(sm.wq) + kk * 6144, 128, kSwizzleNone, 3072), idesc2, kk != 0);
+      mma_commit(&sm.qkv_full);
+    }
+  } else {
+    // ------------------------------------------------- converters, then epilogue
+    const int m = threadIdx.x;
+    const int ihl = m >> 4, iwl = m & 15;
+    const int ih = ih0 + ihl, iw = iw0 + iwl;
+    const bool valid = ih < a.nh && iw < a.nw;
+    const int s = valid ? ih * a.nw + iw : 0;
+    const bool masked = valid && a.rank[b * a.ns + s] >= 0;
+    const bool last_slice = it == a.D.nt - 1;
+    for (int st = 0; st < nst; ++st) {
+      const int ps = st % kNst;
+      mbar_wait(&sm.full[ps], (st / kNst) & 1);
+      const bool zero = last_slice && (st / 8) == T - 1 && masked;   // corrupted frame
+      uint8_t* arow = sm.a[ps] + m * 16;
+#pragma unroll
+      for (int pyl = 0; pyl < 2; ++pyl) {
+        const uint4* src =
+            reinterpret_cast<const uint4*>(sm.u8[ps] + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+          uint4 v = zero ? make_uint4(0, 0, 0, 0) : src[q];
+          const int ki = (pyl * 16 * C + q * 16) / 8;
+          uint4 h0, h1;
+          h0.x = u8x2_to_h2(v.x, 0x4140); h0.y = u8x2_to_h2(v.x, 0x4342);
+          h0.z = u8x2_to_h2(v.y, 0x4140); h0.w = u8x2_to_h2(v.y, 0x4342);
+          h1.x = u8x2_to_h2(v.z, 0x4140); h1.y = u8x2_to_h2(v.z, 0x4342);
+          h1.z = u8x2_to_h2(v.w, 0x4140); h1.w = u8x2_to_h2(v.w, 0x4342);
+          *reinterpret_cast<uint4*>(arow + ki * 2048) = h0;
+          *reinterpret_cast<uint4*>(arow + (ki + 1) * 2048) = h1;
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(&sm.aready[ps]);
+    }
+    // ---- epilogue 1: x = acc/255 + bias + time_pos (+ mask term) ------------
+    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+    mbar_wait(&sm.acc_full, 0);
+    tc_fence_after();
+    float x[64];
+    {
+      uint32_t r[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tmem_ld32(tmem + lane_off + 32 * h, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[32 * h + j] = __uint_as_float(r[j]);
+      }
+    }
+    const bool mterm = last_slice && masked;
+    const float inv255 = 1.f / 255.f;
+#pragma unroll
+    for (int o = 0; o < 64; ++o) {
+      float v = fmaf(x[o], inv255, __ldg(a.emb_b + o));
+      if (mterm) v += __ldg(a.emb_wmsum + o);
+      x[o] = v + __ldg(a.time_pos + it * 64 + o);
+    }
+    if (valid) {
+      float4* xo = reinterpret_cast<float4*>(a.x + (size_t(b * a.D.nt + it) * a.ns + s) * 64);
+#pragma unroll
+      for (int o = 0; o < 64; o += 4) xo[o / 4] = make_float4(x[o], x[o + 1], x[o + 2], x[o + 3]);
+    }
+    // ---- LN_s (block 0) in registers -> fp16 A2 -----------------------------
+    float mean = 0.f;
+#pragma unroll
+    for (int o = 0; o < 64; ++o) mean += x[o];
+    mean *= (1.f / 64.f);
+    float var = 0.f;
+#pragma unroll
+    for (int o = 0; o < 64; ++o) var = fmaf(x[o] - mean, x[o] - mean, var);
+    const float rstd = rsqrtf(var * (1.f / 64.f) + 1e-5f);
+    uint8_t* a2row = sm.a2 + m * 16;
+#pragma unroll
+    for (int ki = 0; ki < 8; ++ki) {
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int o = ki * 8 + j;
+        y[j] = (x[o] - mean) * rstd * __ldg(a.ln_w + o) + __ldg(a.ln_b + o);
+      }
+      *reinterpret_cast<uint4*>(a2row + ki * 2048) =
+          make_uint4(pack_h2(y[0], y[1]), pack_h2(y[2], y[3]), pack_h2(y[4], y[5]),
+                     pack_h2(y[6], y[7]));
+    }
+    fence_proxy_async();
+    mbar_arrive(&sm.a2_ready);
+    // ---- epilogue 2: q, k, v (+ bias) -> bf16 attention operands -----------
+    mbar_wait(&sm.qkv_full, 0);
+    tc_fence_after();
+    int qrow = s;
+    if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
+#pragma unroll 1
+    for (int c6 = 0; c6 < 6; ++c6) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_off + 64 + 32 * c6, r);
+      tmem_wait_ld();
+      if (!valid) continue;
+      const int which = c6 >> 1, head = c6 & 1;
+      const size_t seq = size_t(b * a.D.nt + it) * 2 + head;
+      float v[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + __ldg(a.qkv_b + 32 * c6 + e);
+      if (which < 2) {
+        if (which == 0 && qrow < 0) continue;
+        __nv_bfloat16* dst = (which == 0 ? a.qh : a.kh) +
+                             (seq * a.ns_pad + (which == 0 ? qrow : s)) * 32;
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int e = 0; e < 32; e += 8)
+          d4[e / 8] = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
+                                 pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
+      } else {
+        __nv_bfloat16* dst = a.vth + seq * 32 * a.ns_pad + s;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) dst[size_t(e) * a.ns_pad] = __float2bfloat16_rn(v[e]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int C>
+cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  // u8 HWC planes viewed as (16c bytes, iw, py, ih, slot)
+  CUtensorMap tm;
+  cuuint64_t dims[5] = {cuuint64_t(16 * C), cuuint64_t(a.nw), 16, cuuint64_t(a.nh),
+                        cuuint64_t(a.n_slots)};
+  cuuint64_t strides[4] = {cuuint64_t(16 * C), cuuint64_t(a.w) * C, cuuint64_t(16) * a.w * C,
+                           cuuint64_t(a.h) * a.w * C};
+  cuuint32_t box[5] = {cuuint32_t(16 * C), kTw, 2, kTh, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(a.frames), dims, strides,
+         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const size_t smem = sizeof(EmbSmem<C>) + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(embed_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const int tiles = ((a.nh + kTh - 1) / kTh) * ((a.nw + kTw - 1) / kTw);
+  embed_tc_kernel<C><<<dim3(tiles, a.D.nt, a.b), kThreads, smem, s>>>(tm, a, *a.tcw);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool embed_tc_supported(const Dims& D) {
+  return D.p == 16 && D.d == 64 && D.heads == 2 && (D.c == 1 || D.c == 3) && D.T <= 2;
+}
+
+cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s) {
+  return a.D.c == 3 ? launch_c<3>(a, s) : launch_c<1>(a, s);
+}
+
+}  // namespace nvrec

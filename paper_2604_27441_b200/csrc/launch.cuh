@@ -61,6 +61,21 @@ struct AttnArgs {
 
 // tensor-core spatial attention envelope (k_attn_tc.cu)
 bool tc_supported(const Dims& D);
+// tensor-core embedding (+ block-0 LN/QKV) envelope (k_embed_tc.cu)
+bool embed_tc_supported(const Dims& D);
+struct EmbedTcArgs {
+  Dims D;
+  const TcW* tcw;                 // host copy of the packed-weight pointers
+  const float* emb_wmsum; const float* emb_b; const float* time_pos;
+  const float* ln_w; const float* ln_b; const float* qkv_b;
+  const uint8_t* frames; const int32_t* frame_index; int n_slots;
+  const int* rank;                // masked patches (block mask), required
+  const int* qrank;               // compact Q rows (block 0 pruned) or null
+  float* x;
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
+  int b, h, w, nh, nw, ns, ns_pad;
+};
+cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 
 cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s);
 cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s);
