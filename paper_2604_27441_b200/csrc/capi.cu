@@ -224,7 +224,23 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     ta.dst.rank = (!last && li + 1 == D.layers - 1 && pruned) ? A.rank : nullptr;
     ta.img_h = h; ta.img_w = w; ta.nh = A.nh; ta.nw = A.nw; ta.ns = A.ns;
     ta.out_f32 = out_f32; ta.out_u8 = out_u8;
-    {
+    if (fast && !last && nvrec::token_tc_supported(D) && m->W.tc.blk[li]) {
+      const nvrec::BlockW& bw = m->W.blk[li];
+      const nvrec::BlockW& bn = m->W.blk[li + 1];
+      nvrec::TokenTcArgs tt{};
+      tt.b = b; tt.ns = A.ns; tt.ns_pad = A.ns_pad; tt.nt = D.nt;
+      tt.x = A.x; tt.ao = A.ao;
+      tt.w_blk = m->W.tc.blk[li];
+      tt.w_qkv_next = m->W.tc.blk[li + 1] + 53248;
+      tt.b_proj_s = bw.proj_s_b; tt.ln_t_w = bw.ln_t_w; tt.ln_t_b = bw.ln_t_b;
+      tt.b_qkv_t = bw.qkv_t_b; tt.b_proj_t = bw.proj_t_b; tt.ln_m_w = bw.ln_m_w;
+      tt.ln_m_b = bw.ln_m_b; tt.b_fc1 = bw.fc1_b; tt.b_fc2 = bw.fc2_b;
+      tt.ln_s_next_w = bn.ln_s_w; tt.ln_s_next_b = bn.ln_s_b; tt.b_qkv_next = bn.qkv_s_b;
+      tt.qh = A.qh; tt.kh = A.kh; tt.vth = A.vth;
+      tt.qrank = ta.dst.rank;
+      ProfScope ps(NVREC_STAGE_TOKEN, s);
+      e = nvrec::launch_token_tc(tt, s);
+    } else {
       ProfScope ps(NVREC_STAGE_TOKEN, s);
       e = nvrec::launch_token(ta, b, A.ns, s);
     }
@@ -383,12 +399,26 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     }
     const float* q0 = t[3 + 2];                      // blocks.0.attn_s.qkv.weight (3d, d)
     size_t qoff = pack(3 * d, d, [&](int n, int k) { return q0[size_t(n) * d + k]; });
+    std::vector<size_t> blk_pack;
+    for (int i = 0; i < D.layers; ++i) {
+      const float* const* bt = t + 3 + 18 * i;
+      auto lin = [&](const float* wt, int N, int K) {
+        return pack(N, K, [&](int n, int k) { return wt[size_t(n) * K + k]; });
+      };
+      blk_pack.push_back(lin(bt[4], d, d));            // attn_s.proj
+      lin(bt[8], 3 * d, d);                            // attn_t.qkv
+      lin(bt[10], d, d);                               // attn_t.proj
+      lin(bt[14], 4 * d, d);                           // mlp.0
+      lin(bt[16], d, 4 * d);                           // mlp.2
+      lin(bt[2], 3 * d, d);                            // attn_s.qkv
+    }
     CK(cudaMalloc(&m->blob_bf16, hb.size() * sizeof(__half)), "cudaMalloc(fp16)");
     CK(cudaMemcpy(m->blob_bf16, hb.data(), hb.size() * sizeof(__half),
                   cudaMemcpyHostToDevice), "cudaMemcpy(fp16)");
     m->W.tc.emb = m->blob_bf16 + stage_off[0];
     m->W.tc.emb_stage_elems = d * kst;
     m->W.tc.qkv0 = m->blob_bf16 + qoff;
+    for (int i = 0; i < D.layers; ++i) m->W.tc.blk[i] = m->blob_bf16 + blk_pack[i];
   }
   m->loaded = true;
   return 0;

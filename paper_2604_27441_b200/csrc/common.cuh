@@ -44,6 +44,9 @@ struct TcW {
   const __half* emb;            // [T*8 stages][64 x 32c] embed weight blocks
   const __half* qkv0;           // [192 x 64] block-0 qkv_s weight
   int emb_stage_elems;          // 64 * 32c
+  // per block, contiguous: proj_s [64x64] | qkv_t [192x64] | proj_t [64x64] |
+  // fc1 [256x64] | fc2 [64x256] | qkv_s [192x64]
+  const __half* blk[8];
 };
 
 struct ModelW {

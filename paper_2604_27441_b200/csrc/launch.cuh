@@ -77,6 +77,20 @@ struct EmbedTcArgs {
 };
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 
+// tensor-core tail of a non-last block (k_token_tc.cu)
+bool token_tc_supported(const Dims& D);
+struct TokenTcArgs {
+  int b, ns, ns_pad, nt;
+  float* x; const float* ao;
+  const __half* w_blk;          // this block's fp16 pack (proj_s..fc2)
+  const __half* w_qkv_next;     // next block's qkv_s pack
+  const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
+  const float *b_fc1, *b_fc2, *ln_s_next_w, *ln_s_next_b, *b_qkv_next;
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
+  const int* qrank;             // compact Q rows for a pruned next block, or null
+};
+cudaError_t launch_token_tc(const TokenTcArgs& a, cudaStream_t s);
+
 cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s);
 cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s);
 cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index, int F,

@@ -68,7 +68,9 @@ class MaskedVideoModel(nn.Module):
     # -- weights -> device ----------------------------------------------------
 
     def _signature(self):
-        return tuple((id(v), v.data_ptr(), v._version) for v in self.state_dict().values())
+        # parameters are stable objects: in-place updates (load_state_dict,
+        # optimiser steps) bump _version, re-assignment changes data_ptr
+        return tuple((v.data_ptr(), v._version) for v in self.parameters())
 
     def native(self, device=None) -> _native.NativeModel:
         """The packed on-device model, re-packed when any parameter changed."""
