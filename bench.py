@@ -49,8 +49,8 @@ MODS = (("rgb", 3, 1024), ("depth", 1, 512))      # name, channels, shard L
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams-per-gpu", type=int, default=8)
     ap.add_argument("--precision", default="fast", choices=["fast", "precise"])
@@ -78,7 +78,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q,
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
@@ -137,6 +137,8 @@ class ModalityWork:
             for i in range(F):
                 hf[s * F + i] = tex[i % 8: i % 8 + H, 0:W]      # slow drift
         self.frames = self.host_frames.to(device)
+        self.ring_view = self.frames.view(S, F, H, W, c)
+        self.host_planes = self.host_frames.view(S, F, H, W, c)[:, -1].contiguous().pin_memory()
         self.index = torch.tensor([[s * F + i for i in stack_slots(5, 5, F)]
                                    for s in range(S)], dtype=torch.int32, device=device)
         # loss-mask jobs: GE-dropped body shards of synthetic P-frame headers
@@ -170,13 +172,29 @@ class ModalityWork:
         self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
 
     def e2e_step(self, stream):
-        """Same step through pinned host buffers (H2D in, D2H out)."""
+        """Streaming in-process backend through pinned host buffers: the
+        receiver hands over each stream's decoded corrupted plane and its
+        loss-mask job (H2D); the k references are the device-resident ring
+        of earlier displayable planes; the recovered plane is pushed into the
+        ring (D2D) and returned to the host (D2H)."""
         self.lm.launch(stream)                               # H2D jobs + kernel
+        self.ring_view[:, -1].copy_(self.host_planes, non_blocking=True)
+        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+        self.ring_view[:, -2].copy_(self.out, non_blocking=True)   # ring push
+        self.host_out.copy_(self.out, non_blocking=True)
+
+    def protocol_step(self, stream):
+        """Reference wire-protocol semantics (recovery.py:219-227): every
+        request ships the corrupted plane AND all k references (H2D)."""
+        self.lm.launch(stream)
         self.frames.copy_(self.host_frames, non_blocking=True)
         self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
         self.host_out.copy_(self.out, non_blocking=True)
 
     def h2d_bytes(self):
+        return int(self.lm.h2d_bytes + self.host_planes.numel())
+
+    def h2d_bytes_protocol(self):
         return int(self.lm.h2d_bytes + self.host_frames.numel())
 
     def d2h_bytes(self):
@@ -316,12 +334,16 @@ def main():
     clocks = ClockSampler(local)
     ms = timed(works, streams, "device_step", args.steps, dist_on)
     clk = clocks.stop()
-    # end-to-end through host buffers
+    # end-to-end through host buffers (streaming backend) and the reference
+    # wire-protocol variant that re-ships all k references every request
     ms_e2e = timed(works, streams, "e2e_step", args.steps, dist_on)
-    # per-stage device times (separate pass with event brackets)
+    ms_proto = timed(works, streams, "protocol_step", max(3, args.steps // 4), dist_on)
+    # per-stage device times: separate pass, both modalities serialised on ONE
+    # stream so event brackets are not inflated by the concurrent modality
     torch.cuda.synchronize()
+    one = [torch.cuda.current_stream(device)] * len(works)
     with _native.StageProfile() as prof:
-        run_steps(works, streams, "device_step", args.steps)
+        run_steps(works, one, "device_step", args.steps)
         torch.cuda.synchronize()
 
     # single-stream RGB-D latency (b = 1 per modality, e2e through host buffers)
@@ -335,6 +357,8 @@ def main():
             lat.append(timed(single, sst, "e2e_step", 1, False))
         lat_dev = [timed(single, sst, "device_step", 1, False)
                    for _ in range(args.latency_iters)]
+        lat_proto = [timed(single, sst, "protocol_step", 1, False)
+                     for _ in range(args.latency_iters)]
 
     if dist_on:
         torch.distributed.barrier()
@@ -382,15 +406,27 @@ def main():
         "clocks": clk,
         "e2e": {"value": e2e, "unit": "frames/s",
                 "h2d_bytes_per_step": sum(wk.h2d_bytes() for wk in works),
-                "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works)},
+                "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works),
+                "path": "in-process streaming backend: pinned H2D of each stream's corrupted "
+                        "plane + loss-mask job, device-resident k=5 reference ring, D2D ring "
+                        "push, D2H of the recovered plane"},
+        "e2e_protocol": {"value": S * world * max(3, args.steps // 4) / (ms_proto / 1000.0),
+                         "unit": "frames/s",
+                         "h2d_bytes_per_step": sum(wk.h2d_bytes_protocol() for wk in works),
+                         "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works),
+                         "path": "reference wire-protocol payload: all k references re-sent "
+                                 "per request (recovery.py:219-227)"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "p50_latency_ms": statistics.median(lat),
         "p99_latency_ms": float(np.percentile(lat, 99)),
         "p50_latency_device_ms": statistics.median(lat_dev),
+        "p50_latency_protocol_ms": statistics.median(lat_proto),
         "latency_note": "single stream, one RGB-D frame (both modalities on two CUDA "
                         "streams), e2e through pinned host buffers incl. H2D of 6 planes "
                         "per modality and D2H of the result",
         "stage_ms_per_step": {k: v / args.steps for k, v in prof.ms.items() if v},
+        "stage_note": "per-stage device ms from CUDA-event brackets, both modalities "
+                      "serialised on one stream (separate pass)",
         "roofline": {"kernel": att_kind, "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,

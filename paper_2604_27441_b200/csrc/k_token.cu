@@ -21,12 +21,13 @@
 namespace nvrec {
 
 
+template <bool kNarrow>
 __global__ void __launch_bounds__(256)
 token_kernel(TokenArgs a) {
   extern __shared__ float smem[];
   const Dims& D = a.D;
   const int d = D.d, nt = D.nt;
-  const int P = max(1, 48 / nt);
+  const int P = a.P;
   const int b = blockIdx.y;
   const int r0 = blockIdx.x * P;
   const int cnt = a.list ? a.count[b] : a.ns;
@@ -39,6 +40,11 @@ token_kernel(TokenArgs a) {
   float* Ts = As + ntok_max * d;       // [ntok][d]
   float* Hs = Ts + ntok_max * d;       // [ntok][4d]
   __shared__ int spos[48];
+  auto gemm = [&](const float* in, int ldi, int ntok_, int K, const float* Wt, const float* bias,
+                  int N, auto epi) {
+    if (kNarrow) tile_gemm_narrow(in, ldi, ntok_, K, Wt, bias, N, epi);
+    else tile_gemm(in, ldi, ntok_, K, Wt, bias, N, epi);
+  };
 
   for (int j = threadIdx.x; j < npos; j += blockDim.x)
     spos[j] = a.list ? a.list[b * a.ns + r0 + j] : r0 + j;
@@ -53,14 +59,14 @@ token_kernel(TokenArgs a) {
   __syncthreads();
 
   // 1. spatial-attention output projection + residual
-  tile_gemm(As, d, ntok, d, a.w.proj_s_w, a.w.proj_s_b, d,
+  gemm(As, d, ntok, d, a.w.proj_s_w, a.w.proj_s_b, d,
             [&](int t, int n, float v) { Xs[t * d + n] += v; });
   __syncthreads();
   // 2-3. LN_t and qkv_t for every slice (keys/values of all slices needed)
   tile_layernorm(Xs, d, Ts, d, ntok, d, a.w.ln_t_w, a.w.ln_t_b);
   __syncthreads();
   const int d3 = 3 * d;
-  tile_gemm(Ts, d, ntok, d, a.w.qkv_t_w, a.w.qkv_t_b, d3,
+  gemm(Ts, d, ntok, d, a.w.qkv_t_w, a.w.qkv_t_b, d3,
             [&](int t, int n, float v) { Hs[t * d3 + n] = v; });
   __syncthreads();
   // 4. temporal attention over nt slices per (position, head)
@@ -100,17 +106,17 @@ token_kernel(TokenArgs a) {
   const int rows = a.last ? npos : ntok;
   auto rowmap = [&](int t) { return a.last ? t * nt + nt - 1 : t; };
   // 5. temporal output projection + residual
-  tile_gemm(As + roff, rld, rows, d, a.w.proj_t_w, a.w.proj_t_b, d,
+  gemm(As + roff, rld, rows, d, a.w.proj_t_w, a.w.proj_t_b, d,
             [&](int t, int n, float v) { Xs[rowmap(t) * d + n] += v; });
   __syncthreads();
   // 6. MLP
   tile_layernorm(Xs + roff, rld, Ts + roff, rld, rows, d, a.w.ln_m_w, a.w.ln_m_b);
   __syncthreads();
   const int d4 = D.hidden;
-  tile_gemm(Ts + roff, rld, rows, d, a.w.fc1_w, a.w.fc1_b, d4,
+  gemm(Ts + roff, rld, rows, d, a.w.fc1_w, a.w.fc1_b, d4,
             [&](int t, int n, float v) { Hs[t * d4 + n] = gelu_erf(v); });
   __syncthreads();
-  tile_gemm(Hs, d4, rows, d4, a.w.fc2_w, a.w.fc2_b, d,
+  gemm(Hs, d4, rows, d4, a.w.fc2_w, a.w.fc2_b, d,
             [&](int t, int n, float v) { Xs[rowmap(t) * d + n] += v; });
   __syncthreads();
 
@@ -123,7 +129,7 @@ token_kernel(TokenArgs a) {
     }
     tile_layernorm(Xs, d, Ts, d, ntok, d, a.wn.ln_s_w, a.wn.ln_s_b);
     __syncthreads();
-    tile_gemm(Ts, d, ntok, d, a.wn.qkv_s_w, a.wn.qkv_s_b, d3, [&](int t, int n, float v) {
+    gemm(Ts, d, ntok, d, a.wn.qkv_s_w, a.wn.qkv_s_b, d3, [&](int t, int n, float v) {
       const int j = t / nt, it = t - j * nt;
       qkv_store(a.dst, b, it, spos[j], n, v);
     });
@@ -133,7 +139,7 @@ token_kernel(TokenArgs a) {
   tile_layernorm(Xs + roff, rld, Ts, d, npos, d, a.norm_w, a.norm_b);
   __syncthreads();
   const int p = D.p, c = D.c, pc = p * c;
-  tile_gemm(Ts, d, npos, d, a.head_w, a.head_b, D.used, [&](int j, int u, float v) {
+  gemm(Ts, d, npos, d, a.head_w, a.head_b, D.used, [&](int j, int u, float v) {
     const float sg = 1.f / (1.f + expf(-v));
     const int py = u / pc, rem = u - py * pc, px = rem / c, ch = rem - px * c;
     const int s = spos[j];
@@ -150,19 +156,27 @@ token_kernel(TokenArgs a) {
   });
 }
 
-size_t token_smem_bytes(const Dims& D) {
-  const int P = 48 / D.nt > 0 ? 48 / D.nt : 1;
+size_t token_smem_bytes(const Dims& D, int P) {
   const size_t ntok = size_t(P) * D.nt;
   const size_t hcols = D.hidden > 3 * D.d ? D.hidden : 3 * D.d;
   return sizeof(float) * (3 * ntok * D.d + ntok * hcols);
 }
 
-cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s) {
-  const int P = max(1, 48 / a.D.nt);
-  size_t smem = token_smem_bytes(a.D);
-  cudaFuncSetAttribute(token_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  dim3 grid(ceil_div(max_rows, P), b);
-  token_kernel<<<grid, 256, smem, s>>>(a);
+cudaError_t launch_token(const TokenArgs& a_in, int b, int max_rows, cudaStream_t s) {
+  TokenArgs a = a_in;
+  // dense blocks: 48 tokens per CTA; the pruned last block walks a short
+  // list of masked patches, so one position per CTA spreads it over the GPU
+  const bool narrow = a.list != nullptr;
+  a.P = narrow ? 1 : max(1, 48 / a.D.nt);
+  size_t smem = token_smem_bytes(a.D, a.P);
+  dim3 grid(ceil_div(max_rows, a.P), b);
+  if (narrow) {
+    cudaFuncSetAttribute(token_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    token_kernel<true><<<grid, 256, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(token_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    token_kernel<false><<<grid, 256, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

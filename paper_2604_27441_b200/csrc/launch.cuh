@@ -49,6 +49,7 @@ struct TokenArgs {
   int img_h, img_w, nh, nw, ns;
   float* out_f32;       // (b, c, h, w) or null
   uint8_t* out_u8;      // (b, h, w, c) or null
+  int P;                // positions per CTA (set by launch_token)
 };
 
 struct AttnArgs {

@@ -57,6 +57,35 @@ __device__ __forceinline__ void tile_gemm(const float* in, int ldi, int ntok, in
   }
 }
 
+// Same contract as tile_gemm with one token per work item (4 columns): used
+// when a CTA holds only a handful of tokens (pruned last block), so the
+// N/4 x ntok items still spread over the whole CTA.
+template <class Epi>
+__device__ __forceinline__ void tile_gemm_narrow(const float* in, int ldi, int ntok, int K,
+                                                 const float* __restrict__ Wt,
+                                                 const float* __restrict__ bias, int N,
+                                                 Epi epi) {
+  const int nq = N >> 2;
+  for (int item = threadIdx.x; item < nq * ntok; item += blockDim.x) {
+    const int cq = item % nq, t = item / nq;
+    const float* a0 = in + t * ldi;
+    const float* w = Wt + cq * 4;
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < K; ++k) {
+      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + size_t(k) * N));
+      const float x0 = a0[k];
+      c0 = fmaf(x0, wv.x, c0); c1 = fmaf(x0, wv.y, c1);
+      c2 = fmaf(x0, wv.z, c2); c3 = fmaf(x0, wv.w, c3);
+    }
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(bias + cq * 4));
+    epi(t, cq * 4 + 0, c0 + bv.x);
+    epi(t, cq * 4 + 1, c1 + bv.y);
+    epi(t, cq * 4 + 2, c2 + bv.z);
+    epi(t, cq * 4 + 3, c3 + bv.w);
+  }
+}
+
 // LayerNorm (eps 1e-5, biased variance, affine) of rows of width d <= 128,
 // one warp per row: out[r*ldo + :] = LN(in[r*ldi + :]).  nn.LayerNorm
 // (model.py:47-52,79).
