@@ -4,21 +4,20 @@
 // time slice, head), non-causal, unmasked, head_dim 32, bf16 operands, fp32
 // scores / softmax / output.
 //
-// CTA = two 128-query tiles (ping-pong) of one (slice, head) sequence;
-// 10 warps:
-//   warps 0-3  softmax of query tile 0    (TMEM lanes 0-127, one row/thread)
-//   warps 4-7  softmax of query tile 1
-//   warp  8    TMA producer: Q tiles once, then K/V tiles through a 3-stage
+// CTA = three 128-query tiles (round-robin on the tensor core) of one
+// (slice, head) sequence; 14 warps:
+//   warps 4t..4t+3  softmax of query tile t (TMEM lanes 0-127, one row/thread)
+//   warp  12   TMA producer: Q tiles once, then K/V tiles through a 3-stage
 //              ring (K: 128 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x 2 x 128 B,
 //              SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
-//   warp  9    MMA issuer (one thread): S_t = Q_t K^T (M128 N128 K32, fp32 in
+//   warp  13   MMA issuer (one thread): S_t = Q_t K^T (M128 N128 K32, fp32 in
 //              TMEM), then PV_t = P_t V (M128 N32 K128, P read from TMEM where
 //              the softmax warps stored it as packed bf16 over S_t)
-// TMEM (512 columns): tile t owns S at [256t, 256t+128) and PV at
-// [256t+128, 256t+160).  Per key tile j a softmax thread loads its S row
-// (128 fp32), folds the previous PV into its register-resident output with
-// the previous rescale factor, computes the online-softmax probabilities in
-// base 2, and stores P (bf16) back into TMEM.  MMAs of one thread execute in
+// TMEM (512 columns): tile t owns S at [128t, 128t+128) and its output O at
+// [384+32t, 416+32t); P V accumulates into O across all key tiles.  Per key
+// tile j a softmax thread loads its S row (128 fp32), rescales O in TMEM only
+// when the running max of a row of its warp moved, computes the online-
+// softmax probabilities in base 2, and stores P (bf16) back over S.  MMAs of one thread execute in
 // issue order, so "S_t(j+1) after PV_tj" needs no extra fence, and the
 // commit after S_t(j+1) also certifies PV_tj.
 //
@@ -40,20 +39,24 @@ constexpr int kHd = 32;
 constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
 constexpr int kStages = 3;
-constexpr int kThreads = 320;
+constexpr int kQT = 3;                                 // query tiles per CTA
+constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
 constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
 constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
 constexpr uint32_t kIdescS = idesc_bf16(128, 128);
+// TMEM: S/P of tile t at [128t, 128t+128), its PV at [384 + 32t, 416 + 32t)
+constexpr uint32_t kColS = 128, kColPV = 384;
+static_assert(kQT * kColS <= kColPV && kColPV + 32 * kQT <= 512, "TMEM budget");
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 
 struct __align__(1024) Smem {
   uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
-  uint8_t q[2][kQBytes];            // 512-aligned (SWIZZLE_64B atoms)
+  uint8_t q[kQT][kQBytes];          // 512-aligned (SWIZZLE_64B atoms)
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[2], p_full[2];
+  uint64_t s_full[kQT], p_full[kQT];
   uint32_t tmem_base;
 };
 
@@ -75,17 +78,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int seq = blockIdx.y;
   const int b = seq / (a.nt * a.heads);
   const int nq = a.count ? a.count[b] : a.ns;
-  const int q0 = blockIdx.x * 2 * kTileQ;
+  const int q0 = blockIdx.x * kQT * kTileQ;
   if (q0 >= nq) return;                                   // uniform across the CTA
   const int nkv = (a.ns + kTileK - 1) / kTileK;
 
-  if (warp == 8 && lane == 0) {
+  const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
+  if (warp == kProducer && lane == 0) {
     mbar_init(&sm.q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < kQT; ++t) {
       mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], 128);
     }
@@ -100,12 +104,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 8) {
+  if (warp == kProducer) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(&sm.q_full, 2 * kQBytes);
-      tma_load_3d(sm.q[0], &tm_q, &sm.q_full, 0, q0, seq);
-      tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, q0 + kTileQ, seq);
+      mbar_expect_tx(&sm.q_full, kQT * kQBytes);
+      for (int t = 0; t < kQT; ++t)
+        tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         mbar_wait(&sm.kv_empty[s], ((j / kStages) & 1) ^ 1);
@@ -115,39 +119,38 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMma) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint64_t qdesc[2][2];
-      for (int t = 0; t < 2; ++t)
+      uint64_t qdesc[kQT][2];
+      for (int t = 0; t < kQT; ++t)
         for (int kk = 0; kk < 2; ++kk)
           qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
       auto issue_s = [&](int t, int s) {
         const uint32_t kb = smem_u32(sm.k[s]);
         for (int kk = 0; kk < 2; ++kk)
-          mma_ss(tmem + 256 * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
+          mma_ss(tmem + kColS * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
                  kIdescS, kk);
         mma_commit(&sm.s_full[t]);
       };
       mbar_wait(&sm.q_full, 0);
       mbar_wait(&sm.kv_full[0], 0);
       tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
+      for (int t = 0; t < kQT; ++t) issue_s(t, 0);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         const bool more = j + 1 < nkv;
         const int s1 = (j + 1) % kStages;
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < kQT; ++t) {
           mbar_wait(&sm.p_full[t], j & 1);
           tc_fence_after();
           const uint32_t vb = smem_u32(sm.v[s]);
           for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
             const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
-            mma_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8,
-                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+            mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
+                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
           }
-          if (t == 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
+          if (t == kQT - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
           if (more) {
             if (t == 0) {
               mbar_wait(&sm.kv_full[s1], ((j + 1) / kStages) & 1);
@@ -166,16 +169,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quarter = warp & 3;            // TMEM lane quarter
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + 256 * t;
-    const uint32_t t_pv = t_s + 128;
-    float o[kHd];
-#pragma unroll
-    for (int e = 0; e < kHd; ++e) o[e] = 0.f;
-    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+    const uint32_t t_s = tmem + lane_off + kColS * t;
+    const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
+    float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&sm.s_full[t], j & 1);
+      mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
       tc_fence_after();
-      const int valid = a.ns - j * kTileK;   // keys of this tile that exist
+      const int valid = a.ns - j * kTileK;       // keys of this tile that exist
       // pass 1: row max of the raw scores (32-column chunks keep registers low)
       float mx = -INFINITY;
 #pragma unroll
@@ -192,16 +192,17 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             mx = fmaxf(mx, 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
         }
       }
-      // fold the previous tile's P V into the register-resident output
-      if (j > 0) {
-        uint32_t pv[32];
-        tmem_ld32(t_pv, pv);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < kHd; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(pv[e]));
-      }
       const float mn = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - mn);
+      // rescale the TMEM-resident output when any row of the warp moved its max
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        uint32_t ov[32];
+        tmem_ld32(t_o, ov);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < kHd; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+        tmem_st32(t_o, ov);
+      }
       // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
       // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
       // P pairs to columns [16ch, 16ch+16))
@@ -227,20 +228,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
       l = l * alpha + sum;
       m = mn;
-      alpha_prev = alpha;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
     }
-    mbar_wait(&sm.s_full[t], nkv & 1);
+    mbar_wait(&sm.s_full[t], nkv & 1);           // final PV_t done
     tc_fence_after();
-    {
-      uint32_t pv[32];
-      tmem_ld32(t_pv, pv);
-      tmem_wait_ld();
-#pragma unroll
-      for (int e = 0; e < kHd; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(pv[e]));
-    }
+    uint32_t ov[32];
+    tmem_ld32(t_o, ov);
+    tmem_wait_ld();
     const int q = q0 + t * kTileQ + row;
     if (q < nq) {
       const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
@@ -249,7 +245,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
 #pragma unroll
       for (int e = 0; e < kHd; e += 4)
-        dst[e / 4] = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+        dst[e / 4] = make_float4(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv,
+                                 __uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv);
     }
   }
   tc_fence_before();
@@ -316,7 +313,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = true;
   }
-  dim3 grid(ceil_div(A.ns, 2 * kTileQ), seqs);
+  dim3 grid(ceil_div(A.ns, kQT * kTileQ), seqs);
   attn_tc_kernel<<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
   return cudaGetLastError();
 }

@@ -16,30 +16,26 @@
 // slice reaches the head, so its temporal query, proj_t and MLP run for that
 // slice only; on the server path the CTA walks the masked-patch list instead
 // of all positions (the merge discards every other prediction, server.py:196).
+#include <algorithm>
+
 #include "launch.cuh"
 
 namespace nvrec {
 
 
 template <bool kNarrow>
-__global__ void __launch_bounds__(256)
-token_kernel(TokenArgs a) {
-  extern __shared__ float smem[];
+__device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, int cnt,
+                                           float* smem, int* spos) {
   const Dims& D = a.D;
   const int d = D.d, nt = D.nt;
   const int P = a.P;
-  const int b = blockIdx.y;
-  const int r0 = blockIdx.x * P;
-  const int cnt = a.list ? a.count[b] : a.ns;
   const int npos = min(P, cnt - r0);
-  if (npos <= 0) return;
   const int ntok = npos * nt;
   const int ntok_max = P * nt;
   float* Xs = smem;                    // [ntok][d]   token t = j*nt + it
   float* As = Xs + ntok_max * d;       // [ntok][d]
   float* Ts = As + ntok_max * d;       // [ntok][d]
   float* Hs = Ts + ntok_max * d;       // [ntok][4d]
-  __shared__ int spos[48];
   auto gemm = [&](const float* in, int ldi, int ntok_, int K, const float* Wt, const float* bias,
                   int N, auto epi) {
     if (kNarrow) tile_gemm_narrow(in, ldi, ntok_, K, Wt, bias, N, epi);
@@ -156,6 +152,22 @@ token_kernel(TokenArgs a) {
   });
 }
 
+// Dense blocks: one tile per CTA.  The pruned last block: a grid-stride loop
+// over the stream's masked-patch list (the count lives on the device, so the
+// grid is sized for the GPU, not for the worst case).
+template <bool kNarrow>
+__global__ void __launch_bounds__(256)
+token_kernel(TokenArgs a) {
+  extern __shared__ float smem[];
+  __shared__ int spos[48];
+  const int b = blockIdx.y;
+  const int cnt = a.list ? a.count[b] : a.ns;
+  for (int r0 = blockIdx.x * a.P; r0 < cnt; r0 += gridDim.x * a.P) {
+    token_tile<kNarrow>(a, b, r0, cnt, smem, spos);
+    __syncthreads();
+  }
+}
+
 size_t token_smem_bytes(const Dims& D, int P) {
   const size_t ntok = size_t(P) * D.nt;
   const size_t hcols = D.hidden > 3 * D.d ? D.hidden : 3 * D.d;
@@ -170,6 +182,7 @@ cudaError_t launch_token(const TokenArgs& a_in, int b, int max_rows, cudaStream_
   a.P = narrow ? 1 : max(1, 48 / a.D.nt);
   size_t smem = token_smem_bytes(a.D, a.P);
   dim3 grid(ceil_div(max_rows, a.P), b);
+  if (narrow) grid.x = std::min<int>(grid.x, std::max(1, 2 * 148 / b));
   if (narrow) {
     cudaFuncSetAttribute(token_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     token_kernel<true><<<grid, 256, smem, s>>>(a);
