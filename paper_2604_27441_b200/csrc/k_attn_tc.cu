@@ -81,6 +81,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int q0 = blockIdx.x * kQT * kTileQ;
   if (q0 >= nq) return;                                   // uniform across the CTA
   const int nkv = (a.ns + kTileK - 1) / kTileK;
+  // query tiles with at least one live row (short compact lists use fewer)
+  const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);
 
   const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
   if (warp == kProducer && lane == 0) {
@@ -107,8 +109,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   if (warp == kProducer) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(&sm.q_full, kQT * kQBytes);
-      for (int t = 0; t < kQT; ++t)
+      mbar_expect_tx(&sm.q_full, ntq * kQBytes);
+      for (int t = 0; t < ntq; ++t)
         tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
@@ -136,12 +138,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&sm.q_full, 0);
       mbar_wait(&sm.kv_full[0], 0);
       tc_fence_after();
-      for (int t = 0; t < kQT; ++t) issue_s(t, 0);
+      for (int t = 0; t < ntq; ++t) issue_s(t, 0);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         const bool more = j + 1 < nkv;
         const int s1 = (j + 1) % kStages;
-        for (int t = 0; t < kQT; ++t) {
+        for (int t = 0; t < ntq; ++t) {
           mbar_wait(&sm.p_full[t], j & 1);
           tc_fence_after();
           const uint32_t vb = smem_u32(sm.v[s]);
@@ -150,7 +152,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
                    sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
           }
-          if (t == kQT - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
+          if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
           if (more) {
             if (t == 0) {
               mbar_wait(&sm.kv_full[s1], ((j + 1) / kStages) & 1);
@@ -172,7 +174,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const uint32_t t_s = tmem + lane_off + kColS * t;
     const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
+    const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
+    for (int j = 0; j < jend; ++j) {
       mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
@@ -232,13 +235,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
     }
-    mbar_wait(&sm.s_full[t], nkv & 1);           // final PV_t done
-    tc_fence_after();
+    if (t < ntq) {
+      mbar_wait(&sm.s_full[t], nkv & 1);         // final PV_t done
+      tc_fence_after();
+    }
     uint32_t ov[32];
     tmem_ld32(t_o, ov);
     tmem_wait_ld();
     const int q = q0 + t * kTileQ + row;
-    if (q < nq) {
+    if (t < ntq && q < nq) {
       const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
       const float inv = 1.f / l;
       float4* dst = reinterpret_cast<float4*>(

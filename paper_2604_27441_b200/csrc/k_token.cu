@@ -38,7 +38,7 @@ __device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, in
   float* Hs = Ts + ntok_max * d;       // [ntok][4d]
   auto gemm = [&](const float* in, int ldi, int ntok_, int K, const float* Wt, const float* bias,
                   int N, auto epi) {
-    if (kNarrow) tile_gemm_narrow(in, ldi, ntok_, K, Wt, bias, N, epi);
+    if (kNarrow) tile_gemm_narrow(in, ldi, ntok_, K, Wt, bias, N, Hs + ntok_max * 4 * d, epi);
     else tile_gemm(in, ldi, ntok_, K, Wt, bias, N, epi);
   };
 
@@ -171,7 +171,7 @@ token_kernel(TokenArgs a) {
 size_t token_smem_bytes(const Dims& D, int P) {
   const size_t ntok = size_t(P) * D.nt;
   const size_t hcols = D.hidden > 3 * D.d ? D.hidden : 3 * D.d;
-  return sizeof(float) * (3 * ntok * D.d + ntok * hcols);
+  return sizeof(float) * (3 * ntok * D.d + ntok * hcols + 256 * 4);   // + split-K scratch
 }
 
 cudaError_t launch_token(const TokenArgs& a_in, int b, int max_rows, cudaStream_t s) {

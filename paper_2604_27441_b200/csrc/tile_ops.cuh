@@ -57,32 +57,50 @@ __device__ __forceinline__ void tile_gemm(const float* in, int ldi, int ntok, in
   }
 }
 
-// Same contract as tile_gemm with one token per work item (4 columns): used
-// when a CTA holds only a handful of tokens (pruned last block), so the
-// N/4 x ntok items still spread over the whole CTA.
+// Same contract as tile_gemm for a CTA holding only a handful of tokens
+// (pruned last block): work items are (token, 4 columns, K slice); the K
+// slices shorten the serial dependence chain ks-fold and are summed through
+// `red` (shared, >= blockDim.x * 4 floats).  All threads must call it.
 template <class Epi>
 __device__ __forceinline__ void tile_gemm_narrow(const float* in, int ldi, int ntok, int K,
                                                  const float* __restrict__ Wt,
                                                  const float* __restrict__ bias, int N,
-                                                 Epi epi) {
+                                                 float* red, Epi epi) {
   const int nq = N >> 2;
-  for (int item = threadIdx.x; item < nq * ntok; item += blockDim.x) {
-    const int cq = item % nq, t = item / nq;
-    const float* a0 = in + t * ldi;
-    const float* w = Wt + cq * 4;
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < K; ++k) {
-      const float4 wv = __ldg(reinterpret_cast<const float4*>(w + size_t(k) * N));
-      const float x0 = a0[k];
-      c0 = fmaf(x0, wv.x, c0); c1 = fmaf(x0, wv.y, c1);
-      c2 = fmaf(x0, wv.z, c2); c3 = fmaf(x0, wv.w, c3);
+  const int items = nq * ntok;
+  int ks = 1;
+  while (ks * 2 * items <= int(blockDim.x) && ks * 2 * 8 <= K) ks *= 2;
+  for (int base = 0; base < items; base += blockDim.x) {
+    const int active = min(items - base, int(blockDim.x) / ks);
+    const int t_id = threadIdx.x;
+    const int it = t_id % active, slice = t_id / active;
+    if (t_id < active * ks) {
+      const int item = base + it;
+      const int cq = item % nq, t = item / nq;
+      const int k0 = slice * (K / ks), k1 = (slice + 1 == ks) ? K : k0 + K / ks;
+      const float* a0 = in + t * ldi;
+      const float* w = Wt + cq * 4;
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const float4 wv = __ldg(reinterpret_cast<const float4*>(w + size_t(k) * N));
+        const float x0 = a0[k];
+        c0 = fmaf(x0, wv.x, c0); c1 = fmaf(x0, wv.y, c1);
+        c2 = fmaf(x0, wv.z, c2); c3 = fmaf(x0, wv.w, c3);
+      }
+      float* r = red + 4 * (slice * active + it);
+      r[0] = c0; r[1] = c1; r[2] = c2; r[3] = c3;
     }
-    const float4 bv = __ldg(reinterpret_cast<const float4*>(bias + cq * 4));
-    epi(t, cq * 4 + 0, c0 + bv.x);
-    epi(t, cq * 4 + 1, c1 + bv.y);
-    epi(t, cq * 4 + 2, c2 + bv.z);
-    epi(t, cq * 4 + 3, c3 + bv.w);
+    __syncthreads();
+    for (int o = threadIdx.x; o < active * 4; o += blockDim.x) {
+      const int it2 = o >> 2, j = o & 3;
+      float acc = 0.f;
+      for (int sl = 0; sl < ks; ++sl) acc += red[4 * (sl * active + it2) + j];
+      const int item = base + it2;
+      const int cq = item % nq, t = item / nq;
+      epi(t, cq * 4 + j, acc + __ldg(bias + cq * 4 + j));
+    }
+    __syncthreads();
   }
 }
 
