@@ -115,12 +115,13 @@ class ModalityWork:
     """S streams of one modality: references + corrupted planes, loss-mask
     jobs, device-resident and pinned-host copies."""
 
-    def __init__(self, name, c, L, S, stream_base, device, precision):
+    def __init__(self, name, c, L, stream_ids, device, precision):
         from paper_2604_27441_b200 import Checkpoint, ModelConfig
         from paper_2604_27441_b200.lossmask import LossMaskBatch, PFrameShards
         from paper_2604_27441_b200.recovery import RecoveryEngine, stack_slots
         from paper_2604_27441_b200.synth import GilbertElliott, p_frame_shards
 
+        S = len(stream_ids)
         self.name, self.c, self.S = name, c, S
         cfg = ModelConfig()
         ck = Checkpoint.random_init(cfg, c, seed=0)          # torch.manual_seed(0) init
@@ -143,9 +144,9 @@ class ModalityWork:
                                    for s in range(S)], dtype=torch.int32, device=device)
         # loss-mask jobs: GE-dropped body shards of synthetic P-frame headers
         jobs = []
-        for s in range(S):
-            ge = GilbertElliott(seed=stream_base + s + 17 * c)
-            hdr, nd, recv, enc = p_frame_shards(np.random.default_rng(stream_base + s + c),
+        for s, sid in enumerate(stream_ids):
+            ge = GilbertElliott(seed=sid + 17 * c)
+            hdr, nd, recv, enc = p_frame_shards(np.random.default_rng(sid + c),
                                                 W, H, c, L, ge.drop, present_ratio=0.1)
             if recv.all():                     # ensure each stream needs recovery
                 recv[1 + (s % max(1, nd - 1))] = False
@@ -324,8 +325,10 @@ def main():
     if dist_on:
         torch.distributed.init_process_group("nccl", device_id=device)
     S = args.streams_per_gpu
-    works = [ModalityWork(n, c, L, S, stream_base=rank * S, device=device,
-                          precision=args.precision) for n, c, L in MODS]
+    from paper_2604_27441_b200.sharding import streams_for_rank
+    mine = streams_for_rank(S * world, rank, world)       # stream s -> GPU s mod N
+    works = [ModalityWork(n, c, L, mine, device=device, precision=args.precision)
+             for n, c, L in MODS]
     streams = [torch.cuda.Stream(device) for _ in works]
 
     # warm-up (both paths), then the device-resident timed region
@@ -349,8 +352,8 @@ def main():
     # single-stream RGB-D latency (b = 1 per modality, e2e through host buffers)
     lat = []
     if rank == 0:
-        single = [ModalityWork(n, c, L, 1, stream_base=999, device=device,
-                               precision=args.precision) for n, c, L in MODS]
+        single = [ModalityWork(n, c, L, [999], device=device, precision=args.precision)
+                  for n, c, L in MODS]
         sst = [torch.cuda.Stream(device) for _ in single]
         run_steps(single, sst, "e2e_step", 5)
         for _ in range(args.latency_iters):

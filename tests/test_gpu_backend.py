@@ -1,0 +1,69 @@
+"""In-process backend (receiver callable) with the device-resident ring."""
+
+from dataclasses import dataclass
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import block_grid, make_state, textured_u8
+from oracle import nvrec_forward, recover as oracle_recover
+
+pytestmark = pytest.mark.gpu
+
+
+@dataclass
+class _Mask:
+    grid: np.ndarray
+
+
+@dataclass
+class _Req:                      # field-compatible with rgbdstream RecoveryRequest
+    frame_id: int
+    modality: int
+    plane: np.ndarray
+    mask: _Mask
+    references: list
+
+
+def _ck(c, seed):
+    from paper_2604_27441_b200 import Checkpoint, ModelConfig
+    arch = nvrec_forward.Arch()
+    st = make_state(arch, c, seed)
+    return Checkpoint(ModelConfig(), c, {k: torch.from_numpy(v) for k, v in st.items()}), st
+
+
+def test_backend_matches_oracle_and_uploads_one_plane_per_frame():
+    from paper_2604_27441_b200.backend import B200Backend
+    ck_d, st_d = _ck(1, 501)
+    be = B200Backend(checkpoint_depth=ck_d)
+    rng = np.random.default_rng(3)
+    frames = textured_u8(rng, 12, 96, 128, 1)[..., 0]
+    ring = [frames[i] for i in range(5)]
+    arch = nvrec_forward.Arch()
+    uploads = []
+    for t in range(5, 12):
+        grid = block_grid(rng, 6, 8, 0.3)
+        grid[0, 0] = True
+        plane = frames[t].copy()
+        resp = be(_Req(t, 1, plane, _Mask(grid), list(ring)))
+        want = oracle_recover.recover(st_d, arch, 1, plane[..., None], grid,
+                                      [r[..., None] for r in ring])[..., 0]
+        assert resp.plane.shape == plane.shape and not resp.fallback
+        assert np.abs(resp.plane.astype(int) - want.astype(int)).max() <= 2
+        uploads.append(be.caches[1].uploads)
+        ring = ring[1:] + [resp.plane]          # receiver.py:268-269
+    # first request uploads its 5 references; afterwards the ring is resident
+    assert uploads[0] == 5 and uploads[-1] == 5
+
+
+def test_backend_echo_rules():
+    from paper_2604_27441_b200.backend import B200Backend
+    ck_r, _ = _ck(3, 502)
+    be = B200Backend(checkpoint_rgb=ck_r)
+    plane = np.full((32, 32, 3), 9, np.uint8)
+    g = np.ones((2, 2), bool)
+    assert np.array_equal(be(_Req(1, 0, plane, _Mask(g), [])).plane, plane)       # no refs
+    assert np.array_equal(be(_Req(1, 0, plane, _Mask(~g), [plane])).plane, plane)  # empty mask
+    dep = np.full((32, 32), 4, np.uint8)
+    assert np.array_equal(be(_Req(1, 1, dep, _Mask(g), [dep])).plane, dep)  # no depth model
