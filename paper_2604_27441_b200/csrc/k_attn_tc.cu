@@ -180,7 +180,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
       // pass 1: row max of the raw scores (32-column chunks keep registers low)
-      float mx = -INFINITY;
+      // (4 independent max chains: the dependent FMNMX chain was a stall source)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
@@ -188,13 +189,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         tmem_wait_ld();
         if (valid >= kTileK) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(r[c]));
+          for (int c = 0; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            mx = fmaxf(mx, 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+            mx4[c & 3] = fmaxf(mx4[c & 3], 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
         }
       }
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float mn = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - mn);
       // rescale the TMEM-resident output when any row of the warp moved its max
@@ -209,7 +211,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
       // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
       // P pairs to columns [16ch, 16ch+16))
-      float sum = 0.f;
+      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32], pk[16];
@@ -222,14 +225,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         }
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(r[c]), a.scale_log2, -mn));
-          const float p1 = ex2(fmaf(__uint_as_float(r[c + 1]), a.scale_log2, -mn));
-          sum += p0 + p1;
-          pk[c >> 1] = pack_bf16(p0, p1);
+          const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                 sc2, nm2);
+          const float2 p = make_float2(ex2(v.x), ex2(v.y));
+          sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+          pk[c >> 1] = pack_bf16(p.x, p.y);
         }
         tmem_st16(t_s + 16 * ch, pk);
       }
-      l = l * alpha + sum;
+      l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
       m = mn;
       tmem_wait_st();
       tc_fence_before();
