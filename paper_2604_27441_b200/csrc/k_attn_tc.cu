@@ -227,7 +227,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 32; c += 2) {
           const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
                                  sc2, nm2);
-          const float2 p = make_float2(ex2(v.x), ex2(v.y));
+          // one pair in four on the FMA pipe, three on MUFU
+          const float2 p = ((c >> 1) & 3) == 3 ? exp2_poly2(v) : make_float2(ex2(v.x), ex2(v.y));
           sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
           pk[c >> 1] = pack_bf16(p.x, p.y);
         }

@@ -205,6 +205,28 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+// 2^v for a pair v <= 0 on the FMA pipe (FA4-style MUFU offload): round to
+// the nearest integer j with the 1.5*2^23 trick, degree-3 polynomial for
+// 2^(v-j) on [-0.5, 0.5] (rel. error 6e-4, below bf16 P's 3.9e-3), then add
+// j to the exponent field.  Since (bits(1.5*2^23) << 23) == 0 mod 2^32, the
+// exponent add is a single IMAD: bits(p) + bits(t) * 2^23.
+__device__ __forceinline__ float2 exp2_poly2(float2 v) {
+  v.x = fmaxf(v.x, -127.f);
+  v.y = fmaxf(v.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 nmagic = make_float2(-12582912.f, -12582912.f);
+  const float2 t = fadd2(v, magic);
+  const float2 j = fadd2(t, nmagic);
+  const float2 f = fadd2(v, make_float2(-j.x, -j.y));
+  float2 p = ffma2(make_float2(0.0555041087f, 0.0555041087f), f,
+                   make_float2(0.2402265070f, 0.2402265070f));
+  p = ffma2(p, f, make_float2(0.6931471806f, 0.6931471806f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(
+      __int_as_float(__float_as_int(p.x) + __float_as_int(t.x) * 8388608),
+      __int_as_float(__float_as_int(p.y) + __float_as_int(t.y) * 8388608));
+}
+
 // MUFU ex2 (approximate, flush-to-zero); ex2(-inf) = +0.
 __device__ __forceinline__ float ex2(float x) {
   float y;
