@@ -47,6 +47,7 @@ struct __align__(128) EmbSmem {
   uint8_t u8[kNst][kU8];
   uint8_t a2[kRows * 64 * 2];
   uint8_t wq[192 * 64 * 2];
+  float par[64 * 5 + 192];        // bias | time_pos[it] | wmsum | ln_w | ln_b | qkv_b
   uint64_t full[kNst], aready[kNst], empty[kNst];
   uint64_t acc_full, wq_full, a2_ready, qkv_full;
   uint32_t tmem_base;
@@ -91,6 +92,14 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     tma_prefetch(&tm_u8);
   }
   if (threadIdx.x < T) sm.slot[threadIdx.x] = a.frame_index[b * a.D.F + it * T + threadIdx.x];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    sm.par[i] = a.emb_b[i];
+    sm.par[64 + i] = a.time_pos[it * 64 + i];
+    sm.par[128 + i] = a.emb_wmsum[i];
+    sm.par[192 + i] = a.ln_w[i];
+    sm.par[256 + i] = a.ln_b[i];
+  }
+  for (int i = threadIdx.x; i < 192; i += blockDim.x) sm.par[320 + i] = a.qkv_b[i];
   if (warp == 0) tmem_alloc<256>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
@@ -190,9 +199,9 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     const float inv255 = 1.f / 255.f;
 #pragma unroll
     for (int o = 0; o < 64; ++o) {
-      float v = fmaf(x[o], inv255, __ldg(a.emb_b + o));
-      if (mterm) v += __ldg(a.emb_wmsum + o);
-      x[o] = v + __ldg(a.time_pos + it * 64 + o);
+      float v = fmaf(x[o], inv255, sm.par[o]);
+      if (mterm) v += sm.par[128 + o];
+      x[o] = v + sm.par[64 + o];
     }
     if (valid) {
       float4* xo = reinterpret_cast<float4*>(a.x + (size_t(b * a.D.nt + it) * a.ns + s) * 64);
@@ -215,7 +224,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int o = ki * 8 + j;
-        y[j] = (x[o] - mean) * rstd * __ldg(a.ln_w + o) + __ldg(a.ln_b + o);
+        y[j] = (x[o] - mean) * rstd * sm.par[192 + o] + sm.par[256 + o];
       }
       *reinterpret_cast<uint4*>(a2row + ki * 2048) =
           make_uint4(pack_h2(y[0], y[1]), pack_h2(y[2], y[3]), pack_h2(y[4], y[5]),
@@ -238,7 +247,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       const size_t seq = size_t(b * a.D.nt + it) * 2 + head;
       float v[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + __ldg(a.qkv_b + 32 * c6 + e);
+      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + sm.par[320 + 32 * c6 + e];
       if (which < 2) {
         if (which == 0 && qrow < 0) continue;
         __nv_bfloat16* dst = (which == 0 ? a.qh : a.kh) +

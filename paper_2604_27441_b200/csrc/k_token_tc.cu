@@ -32,11 +32,16 @@ constexpr uint32_t kWBlockElems = 53248;          // proj_s..fc2 of one block
 constexpr uint32_t kOffProjS = 0, kOffQkvT = 4096, kOffProjT = 16384, kOffFc1 = 20480,
                    kOffFc2 = 36864, kOffQkvS = 53248;
 constexpr int kXStride = 68;                      // fp32 exchange row (bank spread)
+// staged parameter vectors (floats): offsets into TokSmem::par
+constexpr int kPBProjS = 0, kPLnTw = 64, kPLnTb = 128, kPBQkvT = 192, kPBProjT = 384,
+              kPLnMw = 448, kPLnMb = 512, kPBFc1 = 576, kPBFc2 = 832, kPLnSw = 896,
+              kPLnSb = 960, kPBQkvN = 1024, kParFloats = 1216;
 
 struct __align__(128) TokSmem {
   __half w[kOffQkvS + 12288];     // 128 KB of weights
   uint8_t a[128 * 64 * 2];        // 16 KB fp16 A operand (K = 64)
   uint8_t h[128 * 256 * 2];       // 64 KB fp16 hidden (K = 256) / fp32 k,v exchange
+  float par[kParFloats];          // biases + LN affine, staged once per CTA
   uint64_t bar_w, bar_a, bar_d;
   uint32_t tmem_base;
 };
@@ -66,7 +71,7 @@ __device__ __forceinline__ void layernorm64(const float* x, float* y, const floa
   for (int o = 0; o < 64; ++o) var = fmaf(x[o] - mean, x[o] - mean, var);
   const float rstd = rsqrtf(var * (1.f / 64.f) + 1e-5f);
 #pragma unroll
-  for (int o = 0; o < 64; ++o) y[o] = (x[o] - mean) * rstd * __ldg(g + o) + __ldg(bt + o);
+  for (int o = 0; o < 64; ++o) y[o] = (x[o] - mean) * rstd * g[o] + bt[o];
 }
 
 __device__ __forceinline__ void named_sync() {
@@ -127,6 +132,18 @@ token_tc_kernel(TokenTcArgs a) {
       }
     }
   } else {
+    {
+      const struct { const float* src; int off, n; } vecs[12] = {
+          {a.b_proj_s, kPBProjS, 64}, {a.ln_t_w, kPLnTw, 64}, {a.ln_t_b, kPLnTb, 64},
+          {a.b_qkv_t, kPBQkvT, 192}, {a.b_proj_t, kPBProjT, 64}, {a.ln_m_w, kPLnMw, 64},
+          {a.ln_m_b, kPLnMb, 64}, {a.b_fc1, kPBFc1, 256}, {a.b_fc2, kPBFc2, 64},
+          {a.ln_s_next_w, kPLnSw, 64}, {a.ln_s_next_b, kPLnSb, 64}, {a.b_qkv_next, kPBQkvN, 192}};
+#pragma unroll 1
+      for (int v = 0; v < 12; ++v)
+        for (int i = threadIdx.x; i < vecs[v].n; i += 128) sm.par[vecs[v].off + i] = vecs[v].src[i];
+      named_sync();
+    }
+    const float* P_ = sm.par;
     const int m = threadIdx.x;                       // row == TMEM lane
     const uint32_t lane_off = uint32_t(warp * 32) << 16;
     const int j = m / nt, it = m - j * nt;           // position slot, slice
@@ -148,7 +165,7 @@ token_tc_kernel(TokenTcArgs a) {
         tmem_ld32(tmem + lane_off + col + 32 * h, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) x[32 * h + e] += __uint_as_float(r[e]) + __ldg(bias + 32 * h + e);
+        for (int e = 0; e < 32; ++e) x[32 * h + e] += __uint_as_float(r[e]) + bias[32 * h + e];
       }
     };
     const float scale = rsqrtf(32.f);
@@ -174,9 +191,9 @@ token_tc_kernel(TokenTcArgs a) {
       put_row64(sm.a, m, y);
       signal_a();
       wait_d();
-      add64(x, kD64, a.b_proj_s);
+      add64(x, kD64, P_ + kPBProjS);
       // ---- 2. qkv_t(LN_t(x)) -------------------------------------------------
-      layernorm64(x, y, a.ln_t_w, a.ln_t_b);
+      layernorm64(x, y, P_ + kPLnTw, P_ + kPLnTb);
       put_row64(sm.a, m, y);
       signal_a();
       wait_d();
@@ -188,7 +205,7 @@ token_tc_kernel(TokenTcArgs a) {
           tmem_ld32(tmem + lane_off + kD192 + 32 * h, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) y[32 * h + e] = __uint_as_float(r[e]) + __ldg(a.b_qkv_t + 32 * h + e);
+          for (int e = 0; e < 32; ++e) y[32 * h + e] = __uint_as_float(r[e]) + P_[kPBQkvT + 32 * h + e];
         }
       }
       float* xch = reinterpret_cast<float*>(sm.h);   // [128][kXStride]: k(32) | v(32)
@@ -199,12 +216,12 @@ token_tc_kernel(TokenTcArgs a) {
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          xch[m * kXStride + e] = __uint_as_float(r[e]) + __ldg(a.b_qkv_t + 64 + 32 * hh + e);
+          xch[m * kXStride + e] = __uint_as_float(r[e]) + P_[kPBQkvT + 64 + 32 * hh + e];
         tmem_ld32(tmem + lane_off + kD192 + 128 + 32 * hh, r);      // v, head hh
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          xch[m * kXStride + 32 + e] = __uint_as_float(r[e]) + __ldg(a.b_qkv_t + 128 + 32 * hh + e);
+          xch[m * kXStride + 32 + e] = __uint_as_float(r[e]) + P_[kPBQkvT + 128 + 32 * hh + e];
         named_sync();
         float sc[8];
         float mx = -INFINITY;
@@ -259,9 +276,9 @@ token_tc_kernel(TokenTcArgs a) {
       // ---- 3. x += proj_t(o) ---------------------------------------------------
       signal_a();
       wait_d();
-      add64(x, kD64, a.b_proj_t);
+      add64(x, kD64, P_ + kPBProjT);
       // ---- 4. h = GELU(fc1(LN_m(x))) -------------------------------------------
-      layernorm64(x, y, a.ln_m_w, a.ln_m_b);
+      layernorm64(x, y, P_ + kPLnMw, P_ + kPLnMb);
       put_row64(sm.a, m, y);
       signal_a();
       wait_d();
@@ -272,7 +289,7 @@ token_tc_kernel(TokenTcArgs a) {
         tmem_wait_ld();
         float g[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) g[e] = gelu_erf(__uint_as_float(r[e]) + __ldg(a.b_fc1 + 32 * c8 + e));
+        for (int e = 0; e < 32; ++e) g[e] = gelu_erf(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           *reinterpret_cast<uint4*>(sm.h + (4 * c8 + q) * 2048 + m * 16) =
@@ -282,14 +299,14 @@ token_tc_kernel(TokenTcArgs a) {
       signal_a();
       wait_d();
       // ---- 5. x += fc2(h); store x -----------------------------------------------
-      add64(x, kD64, a.b_fc2);
+      add64(x, kD64, P_ + kPBFc2);
       if (valid) {
         float4* xo = reinterpret_cast<float4*>(a.x + xrow);
 #pragma unroll
         for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
       }
       // ---- 6. next block's LN_s + qkv_s -> bf16 attention operands ----------------
-      layernorm64(x, y, a.ln_s_next_w, a.ln_s_next_b);
+      layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
       put_row64(sm.a, m, y);
       signal_a();
       wait_d();
@@ -305,7 +322,7 @@ token_tc_kernel(TokenTcArgs a) {
         const size_t seq = size_t(b * nt + it) * 2 + head;
         float v[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + __ldg(a.b_qkv_next + 32 * c6 + e);
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + P_[kPBQkvN + 32 * c6 + e];
         if (which < 2) {
           if (which == 0 && qrow < 0) continue;
           uint4* d4 = reinterpret_cast<uint4*>((which == 0 ? a.qh : a.kh) +
