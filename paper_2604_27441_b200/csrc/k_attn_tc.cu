@@ -179,34 +179,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
-      // pass 1: row max of the raw scores in 32-column chunks, software-
-      // pipelined: the TMEM load of chunk ch+1 is in flight while chunk ch is
-      // reduced (tcgen05.wait::ld waits for all outstanding loads); four
-      // independent max chains
+      // pass 1: row max of the raw scores (32-column chunks keep registers low)
+      // (4 independent max chains: the dependent FMNMX chain was a stall source)
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      {
-        uint32_t rA[32], rB[32];
-        auto reduce = [&](const uint32_t* r, int ch) {
-          if (valid >= kTileK) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
-          } else {
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(t_s + 32 * ch, r);
+        tmem_wait_ld();
+        if (valid >= kTileK) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              mx4[c & 3] = fmaxf(mx4[c & 3], 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
-          }
-        };
-        tmem_ld32(t_s + 0, rA);
-        tmem_ld32(t_s + 32, rB);
-        tmem_wait_ld();
-        reduce(rA, 0);
-        tmem_ld32(t_s + 64, rA);
-        reduce(rB, 1);
-        tmem_wait_ld();
-        tmem_ld32(t_s + 96, rB);
-        reduce(rA, 2);
-        tmem_wait_ld();
-        reduce(rB, 3);
+          for (int c = 0; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            mx4[c & 3] = fmaxf(mx4[c & 3], 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+        }
       }
       const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float mn = fmaxf(m, mx * a.scale_log2);
@@ -225,40 +213,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       // P pairs to columns [16ch, 16ch+16))
       float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
-      {
-        uint32_t rA[32], rB[32];
-        auto expo = [&](uint32_t* r, int ch) {
-          uint32_t pk[16];
-          if (valid < kTileK) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
-          }
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t r[32], pk[16];
+        tmem_ld32(t_s + 32 * ch, r);
+        tmem_wait_ld();
+        if (valid < kTileK) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
-                                   sc2, nm2);
-            // one pair in four on the FMA pipe, three on MUFU
-            const float2 p = ((c >> 1) & 3) == 3 ? exp2_poly2(v) : make_float2(ex2(v.x), ex2(v.y));
-            sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
-            pk[c >> 1] = pack_bf16(p.x, p.y);
-          }
-          tmem_st16(t_s + 16 * ch, pk);
-        };
-        // same pipelining; P of chunk ch lands on S columns [16ch, 16ch+16),
-        // all of which were consumed by chunks <= ch
-        tmem_ld32(t_s + 0, rA);
-        tmem_wait_ld();
-        tmem_ld32(t_s + 32, rB);
-        expo(rA, 0);
-        tmem_wait_ld();
-        tmem_ld32(t_s + 64, rA);
-        expo(rB, 1);
-        tmem_wait_ld();
-        tmem_ld32(t_s + 96, rB);
-        expo(rA, 2);
-        tmem_wait_ld();
-        expo(rB, 3);
+          for (int c = 0; c < 32; ++c)
+            if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                 sc2, nm2);
+          // one pair in four on the FMA pipe, three on MUFU
+          const float2 p = ((c >> 1) & 3) == 3 ? exp2_poly2(v) : make_float2(ex2(v.x), ex2(v.y));
+          sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+          pk[c >> 1] = pack_bf16(p.x, p.y);
+        }
+        tmem_st16(t_s + 16 * ch, pk);
       }
       l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
       m = mn;
