@@ -67,3 +67,37 @@ def test_backend_echo_rules():
     assert np.array_equal(be(_Req(1, 0, plane, _Mask(~g), [plane])).plane, plane)  # empty mask
     dep = np.full((32, 32), 4, np.uint8)
     assert np.array_equal(be(_Req(1, 1, dep, _Mask(g), [dep])).plane, dep)  # no depth model
+
+
+def test_recovery_pipeline_matches_sequential_engine():
+    """Double-buffered serving loop == per-request engine calls with the
+    receiver's ring semantics (recovered plane joins the ring)."""
+    from paper_2604_27441_b200.lossmask import PFrameShards
+    from paper_2604_27441_b200.recovery import RecoveryEngine, RecoveryPipeline
+    from paper_2604_27441_b200.synth import p_frame_shards
+    from oracle import lossmask as om
+    ck, _ = _ck(3, 503)
+    eng = RecoveryEngine(ck.build_model(), "fast")
+    n, h, w, c, k = 2, 64, 96, 3, 5
+    rng = np.random.default_rng(8)
+    refs = [list(textured_u8(rng, k, h, w, c)) for _ in range(n)]
+    init = torch.from_numpy(np.stack([np.stack(r) for r in refs])).cuda()
+    pipe = RecoveryPipeline(eng, n, h, w, 1024, 2048, 64, init)
+    handles, expected = [], []
+    for step in range(4):
+        planes = np.stack([textured_u8(rng, 1, h, w, c)[0] for _ in range(n)])
+        jobs, outs = [], []
+        for s in range(n):
+            hdr, nd, recv, enc = p_frame_shards(rng, w, h, c, 64, lambda: rng.random() < 0.5,
+                                                present_ratio=0.5)
+            jobs.append(PFrameShards(hdr, nd, recv, 64, enc))
+            grid = om.mask_from_shards(hdr, nd, {i for i in range(nd) if recv[i]}, 64, enc)
+            o = eng.recover(planes[s], grid, refs[s])
+            refs[s] = refs[s][1:] + [o]
+            outs.append(o)
+        expected.append(np.stack(outs))
+        handles.append(pipe.submit(planes, jobs))
+        if step >= 1:
+            got = pipe.result(handles[step - 1])
+            assert np.array_equal(got, expected[step - 1])
+    assert np.array_equal(pipe.result(handles[-1]), expected[-1])
