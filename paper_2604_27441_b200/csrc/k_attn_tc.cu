@@ -7,21 +7,19 @@
 // CTA = three 128-query tiles (round-robin on the tensor core) of one
 // (slice, head) sequence; 14 warps:
 //   warps 4t..4t+3  softmax of query tile t (TMEM lanes 0-127, one row/thread)
-//   warp  12   TMA producer: Q tiles once, then 64-key K/V tiles through a
-//              6-stage ring (K: 64 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x
-//              128 B, SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
-//   warp  13   MMA issuer (one thread): S_tj = Q_t K_j^T (M128 N64 K32, fp32
-//              in TMEM) two key tiles ahead, and PV_tj = P_tj V_j (M128 N32
-//              K64, P read from TMEM where the softmax stored it as packed
-//              bf16 over S_tj) accumulating O_t in TMEM
-// TMEM (512 columns): tile t owns 160 columns at 160t: a double-buffered S/P
-// (+0, +64) and O (+128).  Because S_t(j+1) is computed while the softmax of
-// tile j runs, the softmax never waits for the PV -> S round trip.  Per key
-// tile a softmax thread loads its S row (64 fp32), rescales O in TMEM only
-// when the running max of a row of its warp moved (after PV_t(j-1) is
-// certified by pv_done), computes the online-softmax probabilities in base 2
-// and stores P (bf16) back over S.  MMAs of one thread execute in issue
-// order, so reusing an S buffer right after the PV that reads its P is safe.
+//   warp  12   TMA producer: Q tiles once, then K/V tiles through a 3-stage
+//              ring (K: 128 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x 2 x 128 B,
+//              SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
+//   warp  13   MMA issuer (one thread): S_t = Q_t K^T (M128 N128 K32, fp32 in
+//              TMEM), then PV_t = P_t V (M128 N32 K128, P read from TMEM where
+//              the softmax warps stored it as packed bf16 over S_t)
+// TMEM (512 columns): tile t owns S at [128t, 128t+128) and its output O at
+// [384+32t, 416+32t); P V accumulates into O across all key tiles.  Per key
+// tile j a softmax thread loads its S row (128 fp32), rescales O in TMEM only
+// when the running max of a row of its warp moved, computes the online-
+// softmax probabilities in base 2, and stores P (bf16) back over S.  MMAs of one thread execute in
+// issue order, so "S_t(j+1) after PV_tj" needs no extra fence, and the
+// commit after S_t(j+1) also certifies PV_tj.
 //
 // The score rescale is the dominant cost: 128 MUFU ex2 per row per key tile
 // (the path is exp-bound).
@@ -39,18 +37,17 @@ using namespace sm100;
 
 constexpr int kHd = 32;
 constexpr int kTileQ = 128;
-constexpr int kTileK = 64;                             // keys per S tile
-constexpr int kStages = 6;
+constexpr int kTileK = 128;
+constexpr int kStages = 3;
 constexpr int kQT = 3;                                 // query tiles per CTA
 constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
-constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 4 KB
-constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 4 KB (32 rows x 128 B)
-constexpr uint32_t kIdescS = idesc_bf16(128, kTileK);
-// TMEM per query tile t (160 columns at 160t): S/P double buffer at +0 / +64,
-// output O at +128
-constexpr uint32_t kColTile = 160, kColO = 128;
-static_assert(kQT * kColTile <= 512, "TMEM budget");
+constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
+constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
+constexpr uint32_t kIdescS = idesc_bf16(128, 128);
+// TMEM: S/P of tile t at [128t, 128t+128), its PV at [384 + 32t, 416 + 32t)
+constexpr uint32_t kColS = 128, kColPV = 384;
+static_assert(kQT * kColS <= kColPV && kColPV + 32 * kQT <= 512, "TMEM budget");
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 
 struct __align__(1024) Smem {
@@ -59,7 +56,7 @@ struct __align__(1024) Smem {
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[kQT][2], p_full[kQT], pv_done[kQT];
+  uint64_t s_full[kQT], p_full[kQT];
   uint32_t tmem_base;
 };
 
@@ -95,10 +92,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_init(&sm.kv_empty[s], 1);
     }
     for (int t = 0; t < kQT; ++t) {
-      mbar_init(&sm.s_full[t][0], 1);
-      mbar_init(&sm.s_full[t][1], 1);
+      mbar_init(&sm.s_full[t], 1);
       mbar_init(&sm.p_full[t], 128);
-      mbar_init(&sm.pv_done[t], 1);
     }
     fence_mbar_init();
     tma_prefetch(&tm_q);
@@ -123,6 +118,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
         tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, j * kTileK, seq);
         tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], j * kTileK, 0, seq);
+        tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
       }
     }
   } else if (warp == kMma) {
@@ -132,39 +128,39 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       for (int t = 0; t < kQT; ++t)
         for (int kk = 0; kk < 2; ++kk)
           qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
-      // S_tj = Q_t K_j^T into S buffer (j & 1) of tile t
-      auto issue_s = [&](int t, int j) {
-        const uint32_t kb = smem_u32(sm.k[j % kStages]);
+      auto issue_s = [&](int t, int s) {
+        const uint32_t kb = smem_u32(sm.k[s]);
         for (int kk = 0; kk < 2; ++kk)
-          mma_ss(tmem + kColTile * t + 64 * (j & 1), qdesc[t][kk],
-                 sdesc(kb + kk * 32, 512, kSwizzle64B), kIdescS, kk);
-        mma_commit(&sm.s_full[t][j & 1]);
+          mma_ss(tmem + kColS * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
+                 kIdescS, kk);
+        mma_commit(&sm.s_full[t]);
       };
       mbar_wait(&sm.q_full, 0);
-      // two S tiles ahead: the softmax of tile j+1 never waits for PV_j
-      for (int j0 = 0; j0 < 2 && j0 < nkv; ++j0) {
-        mbar_wait(&sm.kv_full[j0 % kStages], (j0 / kStages) & 1);
-        tc_fence_after();
-        for (int t = 0; t < ntq; ++t) issue_s(t, j0);
-      }
+      mbar_wait(&sm.kv_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < ntq; ++t) issue_s(t, 0);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
-        const bool more = j + 2 < nkv;
+        const bool more = j + 1 < nkv;
+        const int s1 = (j + 1) % kStages;
         for (int t = 0; t < ntq; ++t) {
           mbar_wait(&sm.p_full[t], j & 1);
           tc_fence_after();
           const uint32_t vb = smem_u32(sm.v[s]);
-          for (int kk = 0; kk < 4; ++kk)       // 16 keys per step, 32 B apart
-            mma_ts(tmem + kColTile * t + kColO, tmem + kColTile * t + 64 * (j & 1) + kk * 8,
-                   sdesc(vb + kk * 32, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
-          mma_commit(&sm.pv_done[t]);
+          for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
+            const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+            mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
+                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
+          }
           if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
           if (more) {
             if (t == 0) {
-              mbar_wait(&sm.kv_full[(j + 2) % kStages], ((j + 2) / kStages) & 1);
+              mbar_wait(&sm.kv_full[s1], ((j + 1) / kStages) & 1);
               tc_fence_after();
             }
-            issue_s(t, j + 2);      // reuses buffer (j & 1): after PV_tj in issue order
+            issue_s(t, s1);
+          } else {
+            mma_commit(&sm.s_full[t]);               // final: PV_t(last) done
           }
         }
       }
@@ -175,19 +171,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quarter = warp & 3;            // TMEM lane quarter
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t t_tile = tmem + lane_off + kColTile * t;
-    const uint32_t t_o = t_tile + kColO;
+    const uint32_t t_s = tmem + lane_off + kColS * t;
+    const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
     float m = -INFINITY, l = 0.f;
     const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
     for (int j = 0; j < jend; ++j) {
-      const uint32_t t_s = t_tile + 64 * (j & 1);
-      mbar_wait(&sm.s_full[t][j & 1], (j >> 1) & 1);
+      mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
-      // pass 1: row max of the raw scores (4 independent max chains)
+      // pass 1: row max of the raw scores (32-column chunks keep registers low)
+      // (4 independent max chains: the dependent FMNMX chain was a stall source)
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -203,26 +199,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float mn = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - mn);
-      if (j > 0) {
-        // O must hold PV_t(j-1) before it is rescaled
-        mbar_wait(&sm.pv_done[t], (j - 1) & 1);
-        tc_fence_after();
-        // rescale the TMEM-resident output when any row of the warp moved its max
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          uint32_t ov[32];
-          tmem_ld32(t_o, ov);
-          tmem_wait_ld();
+      // rescale the TMEM-resident output when any row of the warp moved its max
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        uint32_t ov[32];
+        tmem_ld32(t_o, ov);
+        tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < kHd; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-          tmem_st32(t_o, ov);
-        }
+        for (int e = 0; e < kHd; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+        tmem_st32(t_o, ov);
       }
-      // pass 2: p = 2^(s*scale - max) as packed bf16 pairs over the consumed S
-      // columns (chunk ch reads S[32ch, 32ch+32) and writes P to [16ch, 16ch+16))
+      // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
+      // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
+      // P pairs to columns [16ch, 16ch+16))
       float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32], pk[16];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -249,7 +241,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_arrive(&sm.p_full[t]);
     }
     if (t < ntq) {
-      mbar_wait(&sm.pv_done[t], (nkv - 1) & 1);   // final PV_t done
+      mbar_wait(&sm.s_full[t], nkv & 1);         // final PV_t done
       tc_fence_after();
     }
     uint32_t ov[32];
