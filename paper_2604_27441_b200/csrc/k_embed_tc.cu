@@ -34,7 +34,8 @@ using namespace sm100;
 
 constexpr int kRows = 128;
 constexpr int kTh = 8, kTw = 16;   // patch rectangle per CTA
-constexpr int kNst = 3;            // pipeline depth
+constexpr int kNst = 3;            // A/W (MMA operand) ring depth
+constexpr int kNu8 = 6;            // raw-pixel TMA ring depth (prefetch distance)
 constexpr int kThreads = 192;
 
 template <int C>
@@ -44,11 +45,11 @@ struct __align__(128) EmbSmem {
   static constexpr uint32_t kW = 64 * 32 * C * 2;           // fp16 W per stage
   uint8_t a[kNst][kA];
   uint8_t w[kNst][kW];
-  uint8_t u8[kNst][kU8];
+  uint8_t u8[kNu8][kU8];
   uint8_t a2[kRows * 64 * 2];
   uint8_t wq[192 * 64 * 2];
   float par[64 * 5 + 192];        // bias | time_pos[it] | wmsum | ln_w | ln_b | qkv_b
-  uint64_t full[kNst], aready[kNst], empty[kNst];
+  uint64_t u8_full[kNu8], u8_empty[kNu8], w_full[kNst], aready[kNst], empty[kNst];
   uint64_t acc_full, wq_full, a2_ready, qkv_full;
   uint32_t tmem_base;
   int slot[16];
@@ -79,8 +80,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   const int T = a.D.T, nst = T * 8;
 
   if (warp == 4 && lane == 0) {
+    for (int i = 0; i < kNu8; ++i) {
+      mbar_init(&sm.u8_full[i], 1);
+      mbar_init(&sm.u8_empty[i], 128);
+    }
     for (int i = 0; i < kNst; ++i) {
-      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.w_full[i], 1);
       mbar_init(&sm.aready[i], 128);
       mbar_init(&sm.empty[i], 1);
     }
@@ -109,15 +114,24 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   if (warp == 4) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
+      // raw pixels run up to kNu8 stages ahead: their slots free as soon as
+      // the converters have read them
+      for (int st = 0; st < nst; ++st) {
+        const int pu = st % kNu8;
+        mbar_wait(&sm.u8_empty[pu], ((st / kNu8) & 1) ^ 1);
+        mbar_expect_tx(&sm.u8_full[pu], S::kU8);
+        tma_load_5d(sm.u8[pu], &tm_u8, &sm.u8_full[pu], 0, iw0, 2 * (st % 8), ih0,
+                    sm.slot[st / 8]);
+      }
+    } else if (lane == 1) {
+      // weights follow the MMA-operand ring (independent thread, own waits)
       mbar_expect_tx(&sm.wq_full, 192 * 64 * 2);
       bulk_load(sm.wq, tcw.qkv0, 192 * 64 * 2, &sm.wq_full);
       for (int st = 0; st < nst; ++st) {
         const int ps = st % kNst;
         mbar_wait(&sm.empty[ps], ((st / kNst) & 1) ^ 1);
-        mbar_expect_tx(&sm.full[ps], S::kU8 + S::kW);
-        tma_load_5d(sm.u8[ps], &tm_u8, &sm.full[ps], 0, iw0, 2 * (st % 8), ih0,
-                    sm.slot[st / 8]);
-        bulk_load(sm.w[ps], tcw.emb + size_t(st) * tcw.emb_stage_elems, S::kW, &sm.full[ps]);
+        mbar_expect_tx(&sm.w_full[ps], S::kW);
+        bulk_load(sm.w[ps], tcw.emb + size_t(st) * tcw.emb_stage_elems, S::kW, &sm.w_full[ps]);
       }
     }
   } else if (warp == 5) {
@@ -127,6 +141,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       for (int st = 0; st < nst; ++st) {
         const int ps = st % kNst;
         mbar_wait(&sm.aready[ps], (st / kNst) & 1);
+        mbar_wait(&sm.w_full[ps], (st / kNst) & 1);
         tc_fence_after();
         const uint32_t ab = smem_u32(sm.a[ps]), wb = smem_u32(sm.w[ps]);
 #pragma unroll
@@ -156,14 +171,15 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     const bool masked = valid && a.rank[b * a.ns + s] >= 0;
     const bool last_slice = it == a.D.nt - 1;
     for (int st = 0; st < nst; ++st) {
-      const int ps = st % kNst;
-      mbar_wait(&sm.full[ps], (st / kNst) & 1);
+      const int ps = st % kNst, pu = st % kNu8;
+      mbar_wait(&sm.u8_full[pu], (st / kNu8) & 1);
+      if (st >= kNst) mbar_wait(&sm.empty[ps], ((st / kNst) & 1) ^ 1);   // A slot drained
       const bool zero = last_slice && (st / 8) == T - 1 && masked;   // corrupted frame
       uint8_t* arow = sm.a[ps] + m * 16;
 #pragma unroll
       for (int pyl = 0; pyl < 2; ++pyl) {
         const uint4* src =
-            reinterpret_cast<const uint4*>(sm.u8[ps] + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
+            reinterpret_cast<const uint4*>(sm.u8[pu] + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           uint4 v = zero ? make_uint4(0, 0, 0, 0) : src[q];
@@ -177,6 +193,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
           *reinterpret_cast<uint4*>(arow + (ki + 1) * 2048) = h1;
         }
       }
+      mbar_arrive(&sm.u8_empty[pu]);        // raw pixels consumed
       fence_proxy_async();
       mbar_arrive(&sm.aready[ps]);
     }
