@@ -28,16 +28,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Block until the phase with parity `parity` of `bar` has completed.
+// Block until the phase with parity `parity` of `bar` has completed.  The
+// suspend-time hint lets the hardware park the waiting thread until the phase
+// flips instead of re-issuing try_wait: spinning producer/MMA warps otherwise
+// steal issue slots from the softmax/epilogue warps sharing their SMSP.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_LOOP:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra WAIT_DONE;\n\t"
       "bra WAIT_LOOP;\n"
       "WAIT_DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
