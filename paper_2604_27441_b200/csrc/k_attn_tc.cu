@@ -37,23 +37,21 @@ using namespace sm100;
 
 constexpr int kHd = 32;
 constexpr int kTileQ = 128;
-constexpr int kTileK = 96;                             // keys per S tile
-constexpr int kKC = kTileK / 32;                       // 32-column chunks per S row
-constexpr int kStages = 4;
-constexpr int kQT = 4;                                 // query tiles per CTA
+constexpr int kTileK = 128;
+constexpr int kStages = 3;
+constexpr int kQT = 3;                                 // query tiles per CTA
 constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
-constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 6 KB
-constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 6 KB: 3 x (32 dims x 64 B)
-constexpr uint32_t kVChunk = kHd * 64;                 // 32 keys x 32 dims, SWIZZLE_64B
-constexpr uint32_t kIdescS = idesc_bf16(128, kTileK);
-// TMEM: tile t owns 128 columns at 128t: S/P at +0 (96 columns), O at +96
-constexpr uint32_t kColS = 128, kColPV = 96;
-static_assert(kQT * kColS <= 512 && kColPV + 32 <= kColS, "TMEM budget");
+constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
+constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
+constexpr uint32_t kIdescS = idesc_bf16(128, 128);
+// TMEM: S/P of tile t at [128t, 128t+128), its PV at [384 + 32t, 416 + 32t)
+constexpr uint32_t kColS = 128, kColPV = 384;
+static_assert(kQT * kColS <= kColPV && kColPV + 32 * kQT <= 512, "TMEM budget");
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 
 struct __align__(1024) Smem {
-  uint8_t v[kStages][kVBytes];      // 512-aligned (SWIZZLE_64B atoms)
+  uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t q[kQT][kQBytes];          // 512-aligned (SWIZZLE_64B atoms)
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
@@ -119,8 +117,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_wait(&sm.kv_empty[s], ((j / kStages) & 1) ^ 1);
         mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
         tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, j * kTileK, seq);
-        for (int vc = 0; vc < kKC; ++vc)
-          tma_load_3d(sm.v[s] + vc * kVChunk, &tm_v, &sm.kv_full[s], j * kTileK + 32 * vc, 0, seq);
+        tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], j * kTileK, 0, seq);
+        tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
       }
     }
   } else if (warp == kMma) {
@@ -149,10 +147,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           mbar_wait(&sm.p_full[t], j & 1);
           tc_fence_after();
           const uint32_t vb = smem_u32(sm.v[s]);
-          for (int kk = 0; kk < kTileK / 16; ++kk) {   // 16 keys per step: chunk kk/2, +32 B
-            const uint32_t addr = vb + (kk >> 1) * kVChunk + (kk & 1) * 32;
-            mma_ts(tmem + kColS * t + kColPV, tmem + kColS * t + kk * 8,
-                   sdesc(addr, 512, kSwizzle64B), kIdescPV, (j | kk) != 0);
+          for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
+            const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+            mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
+                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
           }
           if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
           if (more) {
@@ -174,7 +172,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_off + kColS * t;
-    const uint32_t t_o = tmem + lane_off + kColS * t + kColPV;
+    const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
     float m = -INFINITY, l = 0.f;
     const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
     for (int j = 0; j < jend; ++j) {
@@ -185,7 +183,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       // (4 independent max chains: the dependent FMNMX chain was a stall source)
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int ch = 0; ch < kKC; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -216,7 +214,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
 #pragma unroll
-      for (int ch = 0; ch < kKC; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32], pk[16];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -307,9 +305,9 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
                    CU_TENSOR_MAP_SWIZZLE_64B) ||
       !make_map_3d(&tk, A.kh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileK,
                    CU_TENSOR_MAP_SWIZZLE_64B) ||
-      // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 32-key boxes (64 B rows)
-      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 32, kHd,
-                   CU_TENSOR_MAP_SWIZZLE_64B))
+      // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 64-key boxes (128 B rows)
+      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 64, kHd,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   TcArgs ta;
   ta.ao = A.ao;
