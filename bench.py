@@ -44,6 +44,7 @@ sys.path.insert(0, ROOT)
 H, W = 720, 1280
 METRIC = "recovered RGB-D frames/sec/GPU and p50 per-frame latency at 720p"
 MODS = (("rgb", 3, 1024), ("depth", 1, 512))      # name, channels, shard L
+MUFU_PEAK = 148 * 16 * 1.965e9                      # ex2/s, derived
 
 
 def parse():
@@ -441,6 +442,13 @@ def main():
     else:
         peak, peak_src = 1590.0, "fallback B200_PROFILING.md"
     achieved = flops / (att_ms / 1000.0) / 1e12 if att_ms else 0.0
+    exps = flops / 128.0                      # 4*hd = 128 MMA-FLOP per score
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "attn_tc_ncu.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get("dram_bytes_per_launch")
+        traffic_src = tj.get("source")
     step_ms_prof = sum(prof.ms.values()) / args.steps
     launches_per_step = prof.total_launches / args.steps
     line = {
@@ -489,7 +497,14 @@ def main():
                       "serialised on one stream (separate pass)",
         "roofline": {"kernel": att_kind, "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
+                     "mufu": {"exp_per_s": exps / (att_ms / 1000.0) if att_ms else 0.0,
+                              "peak_exp_per_s": MUFU_PEAK,
+                              "frac": (exps / (att_ms / 1000.0) / MUFU_PEAK) if att_ms else 0.0,
+                              "note": "binding unit for head_dim 32 (128 MMA-FLOP per exp); "
+                                      "peak = 148 SM x 16 ex2/clk x 1.965 GHz (derived); "
+                                      "1/4 of the exps run as FMA-pipe polynomials"},
                      "share_of_step": att_ms / max(1e-9, sum(prof.ms.values())),
                      "algorithmic_flops_per_launch": flops / max(1, att_launches)},
     }
