@@ -16,6 +16,7 @@
  *   nvrec_forward_f32        <- nvrec/model.py:82-122 MaskedVideoModel.forward
  *   nvrec_recover_u8         <- nvrec/server.py:181-196 RecoveryServer._recover
  *                               (u8 stack/normalise, forward, quantise, merge)
+ *   nvrec_baseline_u8        <- rgbdstream/recovery.py:94-196 recover_baseline
  *   nvrec_loss_mask          <- rgbdstream/receiver.py:224-237 zero-fill +
  *                               rgbdstream/codec.py:159-201,250-257,274-281,
  *                               318-320 (parse_header, block_ranges,
@@ -126,6 +127,17 @@ typedef struct nvrec_lossmask_job {
  * Bit-exact with the reference receiver+codec. */
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream);
 
+/* Timeout / fault fallback on the GPU, bit-exact with the reference
+ * recover_baseline_rgb / recover_baseline_depth (rgbdstream/recovery.py:94-196):
+ * +-8 px SAD block match of every masked 16-px block against the most recent
+ * reference on its intact border ring; depth adds the 3x3 median on the
+ * mask-boundary band.  planes/refs/out: (b, h, w, c) u8 device; mask_bits as
+ * in nvrec_recover_u8.  (No references => the caller returns the plane.) */
+int64_t nvrec_baseline_workspace_bytes(int32_t b, int32_t h, int32_t w, int32_t c);
+int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
+                      const uint8_t* planes, const uint8_t* refs, const uint8_t* mask_bits,
+                      uint8_t* out, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Optional per-stage timing for benchmarks: between begin and end every
  * kernel launch is bracketed by CUDA events on its stream; end synchronises
  * and returns the summed milliseconds and launch counts per NVREC_STAGE_*.
@@ -133,7 +145,8 @@ int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream
 enum {
   NVREC_STAGE_LOSSMASK = 0, NVREC_STAGE_MASKLIST = 1, NVREC_STAGE_COPY = 2,
   NVREC_STAGE_EMBED = 3, NVREC_STAGE_LNQKV = 4, NVREC_STAGE_ATTN_SIMT = 5,
-  NVREC_STAGE_ATTN_TC = 6, NVREC_STAGE_TOKEN = 7, NVREC_NUM_STAGES = 8
+  NVREC_STAGE_ATTN_TC = 6, NVREC_STAGE_TOKEN = 7, NVREC_STAGE_BASELINE = 8,
+  NVREC_NUM_STAGES = 9
 };
 int nvrec_profile_begin(void);
 int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages);

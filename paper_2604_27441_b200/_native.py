@@ -27,9 +27,10 @@ E_INVALID, E_UNSUPPORTED, E_CUDA, E_WORKSPACE, E_STATE = -1, -2, -3, -4, -5
 EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_model_destroy", "nvrec_model_load", "nvrec_workspace_bytes",
            "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask",
-           "nvrec_profile_begin", "nvrec_profile_end")
+           "nvrec_profile_begin", "nvrec_profile_end", "nvrec_baseline_workspace_bytes",
+           "nvrec_baseline_u8")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
-          "token")
+          "token", "baseline")
 
 
 class NativeError(RuntimeError):
@@ -84,6 +85,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_recover_u8.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp, vp,
                                          i64, i32, vp]
         lib.nvrec_loss_mask.argtypes = [vp, i32, vp]
+        lib.nvrec_baseline_workspace_bytes.argtypes = [i32, i32, i32, i32]
+        lib.nvrec_baseline_workspace_bytes.restype = i64
+        lib.nvrec_baseline_u8.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]
         lib.nvrec_profile_end.argtypes = [ctypes.POINTER(ctypes.c_float),
                                           ctypes.POINTER(i32), i32]
         for name in EXPORTS:

@@ -590,6 +590,41 @@ int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream
 }
 
 
+int64_t nvrec_baseline_workspace_bytes(int32_t b, int32_t h, int32_t w, int32_t c) {
+  if (b < 1 || h < 16 || w < 16 || h % 16 || w % 16 || (c != 1 && c != 3))
+    return fail(NVREC_E_INVALID, "bad baseline shape");
+  const size_t ns = size_t(h / 16) * (w / 16);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return int64_t(al(b * ns * 4) * 2 + al(b * 4) + al(b * 16) + al(size_t(b) * h * w * c));
+}
+
+int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
+                      const uint8_t* planes, const uint8_t* refs, const uint8_t* mask_bits,
+                      uint8_t* out, void* ws, int64_t ws_bytes, void* stream) {
+  const int64_t need = nvrec_baseline_workspace_bytes(b, h, w, c);
+  if (need < 0) return int(need);
+  if (depth && c != 1) return fail(NVREC_E_INVALID, "depth baseline needs c == 1");
+  if (!planes || !refs || !mask_bits || !out) return fail(NVREC_E_INVALID, "null pointer");
+  if (!ws || ws_bytes < need) return fail(NVREC_E_WORKSPACE, "baseline workspace too small");
+  const size_t ns = size_t(h / 16) * (w / 16);
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* p = static_cast<char*>(ws);
+  int* list = reinterpret_cast<int*>(p); p += al(b * ns * 4);
+  int* rank = reinterpret_cast<int*>(p); p += al(b * ns * 4);
+  int* count = reinterpret_cast<int*>(p); p += al(b * 4);
+  int* bbox = reinterpret_cast<int*>(p); p += al(b * 16);
+  uint8_t* base = reinterpret_cast<uint8_t*>(p);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_BASELINE, s);
+    e = nvrec::launch_baseline(depth, b, h, w, c, planes, refs, mask_bits, out, base, list,
+                               rank, count, bbox, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "baseline launch");
+  return 0;
+}
+
 int nvrec_profile_begin(void) {
   if (g_prof_pool.empty()) {
     g_prof_pool.resize(kProfMax);

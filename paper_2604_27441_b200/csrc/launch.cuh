@@ -100,6 +100,10 @@ cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s
 cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s);
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
+cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
+                            const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
+                            uint8_t* base, int* list, int* rank, int* count, int* bbox,
+                            cudaStream_t s);
 cudaError_t launch_masklist(const uint8_t* bits, int b, int nbytes, int ns, int* list,
                             int* rank, int* count, cudaStream_t s);
 

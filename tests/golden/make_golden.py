@@ -31,8 +31,8 @@ REF = "/root/reference/pkg"
 sys.path.insert(0, os.path.join(REF, "src"))
 sys.path.insert(0, os.path.join(REF, "nvrec", "src"))
 
-from golden_cases import (MODEL_CASES, RECOVER_CASES, model_case,  # noqa: E402
-                          recover_case)
+from golden_cases import (BASELINE_CASES, MODEL_CASES, RECOVER_CASES,  # noqa: E402
+                          baseline_case, model_case, recover_case)
 from helpers import digest  # noqa: E402
 
 from nvrec.config import ModelConfig  # noqa: E402
@@ -184,8 +184,26 @@ def gen_lossmask():
           "codec cases", len(extra))
 
 
+def gen_baseline():
+    """Reference timeout/fault fallback (rgbdstream/recovery.py:128-196)."""
+    from rgbdstream.codec import CorruptionMask
+    from rgbdstream.frames import Modality
+    from rgbdstream.recovery import RecoveryRequest, recover_baseline
+    out = {}
+    for name in BASELINE_CASES:
+        c, plane, grid, refs = baseline_case(name)
+        mod = Modality.RGB if c == 3 else Modality.DEPTH
+        resp = recover_baseline(RecoveryRequest(1, mod, plane, CorruptionMask(grid.copy()),
+                                                refs))
+        out[name] = resp.plane
+        out[name + "__digest"] = np.array(digest(plane, grid, *refs))
+        print("baseline", name, resp.plane.shape, int((resp.plane != plane).sum()))
+    np.savez_compressed(os.path.join(HERE, "baseline_golden.npz"), **out)
+
+
 if __name__ == "__main__":
     torch.set_num_threads(8)
-    gen_lossmask()
-    gen_model()
-    gen_recover()
+    import sys as _sys
+    which = _sys.argv[1:] or ["lossmask", "model", "recover", "baseline"]
+    for w in which:
+        globals()["gen_" + w]()

@@ -74,3 +74,31 @@ def recover_case(name):
     plane[pix] = 0                          # zero-filled decode output
     refs = [frames[i] for i in range(nref)]
     return arch, c, state, plane, grid, refs
+
+
+# name -> (channels, h, w, mask ratio, seed, n_refs) for recover_baseline
+# (rgbdstream/recovery.py:128-196); dense masks exercise fully-masked rings
+BASELINE_CASES = {
+    "b_rgb_48x64": (3, 48, 64, 0.3, 41, 2),
+    "b_rgb_96x128_dense": (3, 96, 128, 0.7, 42, 1),
+    "b_rgb_240x320": (3, 240, 320, 0.1, 43, 5),
+    "b_depth_48x64": (1, 48, 64, 0.3, 44, 2),
+    "b_depth_96x128_dense": (1, 96, 128, 0.7, 45, 3),
+    "b_depth_240x320": (1, 240, 320, 0.1, 46, 5),
+    "b_depth_16x16_all": (1, 16, 16, 1.0, 47, 1),
+}
+
+
+def baseline_case(name):
+    c, h, w, ratio, seed, nref = BASELINE_CASES[name]
+    rng = np.random.default_rng(seed)
+    frames = textured_u8(rng, nref + 1, h, w, c)
+    if c == 1:
+        frames = frames[..., 0]
+    grid = block_grid(rng, h // 16, w // 16, ratio)
+    if not grid.any():
+        grid[0, 0] = True
+    plane = frames[-1].copy()
+    pix = np.repeat(np.repeat(grid, 16, 0), 16, 1)
+    plane[pix] = 0
+    return c, plane, grid, [frames[i] for i in range(nref)]

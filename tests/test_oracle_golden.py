@@ -68,3 +68,17 @@ def test_lossmask_oracle_codec_tail_rule():
         g = lossmask.decode_mask(hdr, int(LMASK["x_received_len"][i]),
                                  [tuple(r) for r in rng.reshape(-1, 2)])
         assert np.array_equal(g.reshape(-1), want)
+
+
+BASE = np.load(os.path.join(GOLDEN_DIR, "baseline_golden.npz"))
+
+
+@pytest.mark.parametrize("name", sorted(k for k in BASE.files if "__" not in k))
+def test_baseline_oracle_matches_reference(name):
+    from golden_cases import baseline_case
+    from oracle import baseline
+    c, plane, grid, refs = baseline_case(name)
+    assert str(BASE[name + "__digest"]) == digest(plane, grid, *refs)
+    fn = baseline.baseline_rgb if c == 3 else baseline.baseline_depth
+    got, fb = fn(plane, grid, refs)
+    assert not fb and np.array_equal(got, BASE[name])
