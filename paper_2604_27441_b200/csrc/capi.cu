@@ -456,7 +456,7 @@ static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout
   A.v = at<float>(ws, L.v);
   A.qh = at<__nv_bfloat16>(ws, L.qh);
   A.kh = at<__nv_bfloat16>(ws, L.kh);
-  A.vth = at<__half>(ws, L.vth);
+  A.vth = at<__nv_bfloat16>(ws, L.vth);
   A.list = at<int>(ws, L.list);
   A.rank = at<int>(ws, L.rank);
   A.count = at<int>(ws, L.count);

@@ -73,7 +73,7 @@ struct Act {
   float* v;          // [b*nt*heads][ns_pad][hd]
   __nv_bfloat16* qh; // bf16 path: Q,K [seq][ns_pad][32]; Vt [seq][32][ns_pad]
   __nv_bfloat16* kh;
-  __half* vth;        // fp16 V^T (P V runs in fp16: P from ex2.f16x2)
+  __nv_bfloat16* vth;
   int* list;         // [b][ns] masked positions (ascending) or nullptr = dense
   int* rank;         // [b][ns] position -> row in list, -1 if absent
   int* count;        // [b] entries in list

@@ -37,26 +37,21 @@ using namespace sm100;
 
 constexpr int kHd = 32;
 constexpr int kTileQ = 128;
-constexpr int kTileK = 96;                             // keys per S tile
-constexpr int kKC = kTileK / 32;                       // 32-key chunks per S row / V^T tile
-constexpr int kStages = 4;
+constexpr int kTileK = 128;
+constexpr int kStages = 3;
 constexpr int kQT = 3;                                 // query tiles per CTA
 constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
-constexpr int kVRows = 48;                             // V^T rows: 32 dims + ones row + 15 zero rows
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
-constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 6 KB
-constexpr uint32_t kVChunk = kVRows * 64;              // 48 rows x 32 keys (64 B), SWIZZLE_64B
-constexpr uint32_t kVBytes = kKC * kVChunk;            // 9 KB
-constexpr uint32_t kIdescS = idesc_bf16(128, kTileK);  // bf16 Q, K
-constexpr uint32_t kIdescPV = idesc_f16(128, kVRows);  // fp16 P (TMEM) x fp16 V^T
-// TMEM per query tile (144 columns at 144t): S/P at +0 (96 columns; P as
-// packed fp16 pairs over the first 48), O at +96 (32 columns) and the row sum
-// l at +128 (the ones row of V^T; 16 columns, only the first is used)
-constexpr uint32_t kColTile = 144, kColO = 96, kColL = 128;
-static_assert(kQT * kColTile <= 512, "TMEM budget");
+constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
+constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
+constexpr uint32_t kIdescS = idesc_bf16(128, 128);
+// TMEM: S/P of tile t at [128t, 128t+128), its PV at [384 + 32t, 416 + 32t)
+constexpr uint32_t kColS = 128, kColPV = 384;
+static_assert(kQT * kColS <= kColPV && kColPV + 32 * kQT <= 512, "TMEM budget");
+constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 
 struct __align__(1024) Smem {
-  uint8_t v[kStages][kVBytes];      // 512-aligned (SWIZZLE_64B atoms)
+  uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t q[kQT][kQBytes];          // 512-aligned (SWIZZLE_64B atoms)
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
@@ -89,15 +84,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   // query tiles with at least one live row (short compact lists use fewer)
   const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);
 
-  // rows 32..47 of every V^T chunk: the ones row (row sum l) and zeros.  TMA
-  // only ever writes rows 0..31.  A constant row is swizzle-invariant.
-  for (int i = threadIdx.x; i < kStages * kKC * 16 * 32; i += blockDim.x) {
-    const int key = i & 31, r = (i >> 5) & 15, chunk = i >> 9;
-    __half* row = reinterpret_cast<__half*>(sm.v[0] + chunk * kVChunk + (32 + r) * 64);
-    row[key] = __float2half_rn(r == 0 ? 1.f : 0.f);
-  }
-  fence_proxy_async();
-
   const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
   if (warp == kProducer && lane == 0) {
     mbar_init(&sm.q_full, 1);
@@ -129,10 +115,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       for (int j = 0; j < nkv; ++j) {
         const int s = j % kStages;
         mbar_wait(&sm.kv_empty[s], ((j / kStages) & 1) ^ 1);
-        mbar_expect_tx(&sm.kv_full[s], kKBytes + kKC * 32 * 64);
+        mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
         tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, j * kTileK, seq);
-        for (int vc = 0; vc < kKC; ++vc)
-          tma_load_3d(sm.v[s] + vc * kVChunk, &tm_v, &sm.kv_full[s], j * kTileK + 32 * vc, 0, seq);
+        tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], j * kTileK, 0, seq);
+        tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
       }
     }
   } else if (warp == kMma) {
@@ -145,7 +131,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       auto issue_s = [&](int t, int s) {
         const uint32_t kb = smem_u32(sm.k[s]);
         for (int kk = 0; kk < 2; ++kk)
-          mma_ss(tmem + kColTile * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
+          mma_ss(tmem + kColS * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
                  kIdescS, kk);
         mma_commit(&sm.s_full[t]);
       };
@@ -161,11 +147,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           mbar_wait(&sm.p_full[t], j & 1);
           tc_fence_after();
           const uint32_t vb = smem_u32(sm.v[s]);
-          // [O | l] += P V^T_ext : M128 N48, 16 keys per step (chunk kk/2, +32 B)
-          for (int kk = 0; kk < kTileK / 16; ++kk)
-            mma_ts(tmem + kColTile * t + kColO, tmem + kColTile * t + kk * 8,
-                   sdesc(vb + (kk >> 1) * kVChunk + (kk & 1) * 32, 512, kSwizzle64B),
-                   kIdescPV, (j | kk) != 0);
+          for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
+            const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+            mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
+                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
+          }
           if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
           if (more) {
             if (t == 0) {
@@ -185,18 +171,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quarter = warp & 3;            // TMEM lane quarter
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + kColTile * t;
-    const uint32_t t_o = t_s + kColO;
-    float m = -INFINITY;
+    const uint32_t t_s = tmem + lane_off + kColS * t;
+    const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
+    float m = -INFINITY, l = 0.f;
     const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
     for (int j = 0; j < jend; ++j) {
       mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
-      // pass 1: row max of the raw scores (4 independent max chains)
+      // pass 1: row max of the raw scores (32-column chunks keep registers low)
+      // (4 independent max chains: the dependent FMNMX chain was a stall source)
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int ch = 0; ch < kKC; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -212,7 +199,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float mn = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - mn);
-      // rescale the TMEM-resident [O | l] when any row of the warp moved its max
+      // rescale the TMEM-resident output when any row of the warp moved its max
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
         uint32_t ov[32];
         tmem_ld32(t_o, ov);
@@ -220,19 +207,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
 #pragma unroll
         for (int e = 0; e < kHd; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
         tmem_st32(t_o, ov);
-        uint32_t lv[1];
-        tmem_ld1(t_o + 32, lv);
-        tmem_wait_ld();
-        lv[0] = __float_as_uint(__uint_as_float(lv[0]) * alpha);
-        tmem_st1(t_o + 32, lv);
       }
-      // pass 2: p = 2^(s*scale - max): the argument pair goes to f16x2 and one
-      // MUFU ex2.f16x2 yields both probabilities as packed fp16 -- the P
-      // operand itself; written over the consumed S columns (chunk ch reads
-      // S[32ch, 32ch+32) and writes P pairs to [16ch, 16ch+16))
+      // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
+      // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
+      // P pairs to columns [16ch, 16ch+16))
+      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
 #pragma unroll
-      for (int ch = 0; ch < kKC; ++ch) {
+      for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32], pk[16];
         tmem_ld32(t_s + 32 * ch, r);
         tmem_wait_ld();
@@ -245,10 +227,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 32; c += 2) {
           const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
                                  sc2, nm2);
-          pk[c >> 1] = ex2_h2(pack_h2f(v.x, v.y));
+          // one pair in four on the FMA pipe, three on MUFU
+          const float2 p = ((c >> 1) & 3) == 3 ? exp2_poly2(v) : make_float2(ex2(v.x), ex2(v.y));
+          sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+          pk[c >> 1] = pack_bf16(p.x, p.y);
         }
         tmem_st16(t_s + 16 * ch, pk);
       }
+      l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
       m = mn;
       tmem_wait_st();
       tc_fence_before();
@@ -258,14 +244,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&sm.s_full[t], nkv & 1);         // final PV_t done
       tc_fence_after();
     }
-    uint32_t ov[32], lv[1];
+    uint32_t ov[32];
     tmem_ld32(t_o, ov);
-    tmem_ld1(t_o + 32, lv);
     tmem_wait_ld();
     const int q = q0 + t * kTileQ + row;
     if (t < ntq && q < nq) {
       const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
-      const float inv = 1.f / __uint_as_float(lv[0]);
+      const float inv = 1.f / l;
       float4* dst = reinterpret_cast<float4*>(
           a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
 #pragma unroll
@@ -295,15 +280,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                  uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1,
-                 CUtensorMapSwizzle sw,
-                 CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+                 CUtensorMapSwizzle sw) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, dt, 3, const_cast<void*>(base), dims, strides, box,
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -321,9 +305,9 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
                    CU_TENSOR_MAP_SWIZZLE_64B) ||
       !make_map_3d(&tk, A.kh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileK,
                    CU_TENSOR_MAP_SWIZZLE_64B) ||
-      // V^T: [seq][32][ns_pad] fp16 viewed (ns, 32, seq), 32-key boxes (64 B rows)
-      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 32, kHd,
-                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
+      // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 64-key boxes (128 B rows)
+      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 64, kHd,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   TcArgs ta;
   ta.ao = A.ao;

@@ -332,9 +332,9 @@ token_tc_kernel(TokenTcArgs a) {
             d4[e / 8] = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
                                    pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
         } else {
-          __half* dst = a.vth + seq * 32 * a.ns_pad + s;
+          __nv_bfloat16* dst = a.vth + seq * 32 * a.ns_pad + s;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) dst[size_t(e) * a.ns_pad] = __float2half_rn(v[e]);
+          for (int e = 0; e < 32; ++e) dst[size_t(e) * a.ns_pad] = __float2bfloat16_rn(v[e]);
         }
       }
     }

@@ -73,7 +73,7 @@ struct EmbedTcArgs {
   const int* rank;                // masked patches (block mask), required
   const int* qrank;               // compact Q rows (block 0 pruned) or null
   float* x;
-  __nv_bfloat16* qh; __nv_bfloat16* kh; __half* vth;
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
   int b, h, w, nh, nw, ns, ns_pad;
 };
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
@@ -87,7 +87,7 @@ struct TokenTcArgs {
   const __half* w_qkv_next;     // next block's qkv_s pack
   const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
   const float *b_fc1, *b_fc2, *ln_s_next_w, *ln_s_next_b, *b_qkv_next;
-  __nv_bfloat16* qh; __nv_bfloat16* kh; __half* vth;
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
   const int* qrank;             // compact Q rows for a pruned next block, or null
 };
 cudaError_t launch_token_tc(const TokenTcArgs& a, cudaStream_t s);

@@ -145,7 +145,7 @@ __device__ __forceinline__ void tile_layernorm(const float* in, int ldi, float* 
 // token (b, it, s) into the spatial-attention operand layouts.
 struct QkvDst {
   float* q; float* k; float* v;                     // precise (fp32) layouts
-  __nv_bfloat16* qh; __nv_bfloat16* kh; __half* vth;  // fast (bf16 Q/K, fp16 V^T)
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;  // fast (bf16)
   const int* rank;   // non-null: Q rows are compact (pruned consumer block)
   int nt, ns, ns_pad, d, heads, hd;
 };
@@ -163,7 +163,7 @@ __device__ __forceinline__ void qkv_store(const QkvDst& o, int b, int it, int s,
   if (o.qh) {
     if (which == 0) o.qh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
     else if (which == 1) o.kh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
-    else o.vth[(seq * o.hd + e) * o.ns_pad + row] = __float2half_rn(v);
+    else o.vth[(seq * o.hd + e) * o.ns_pad + row] = __float2bfloat16_rn(v);
   } else {
     float* dst = which == 0 ? o.q : (which == 1 ? o.k : o.v);
     dst[(seq * o.ns_pad + row) * o.hd + e] = v;
