@@ -17,6 +17,11 @@
  *   nvrec_recover_u8         <- nvrec/server.py:181-196 RecoveryServer._recover
  *                               (u8 stack/normalise, forward, quantise, merge)
  *   nvrec_baseline_u8        <- rgbdstream/recovery.py:94-196 recover_baseline
+ *   nvrec_decode             <- rgbdstream/codec.py:260-321 decode (zero-fill
+ *                               P-frame / I-frame decode + its mask), fed by
+ *                               receiver.py:222-237 (_finalize_p body)
+ *   nvrec_rs_plan/           <- rgbdstream/fec.py:144-163 rs_reconstruct
+ *   nvrec_rs_reconstruct        (receiver.py:180-209 _finalize_i)
  *   nvrec_loss_mask          <- rgbdstream/receiver.py:224-237 zero-fill +
  *                               rgbdstream/codec.py:159-201,250-257,274-281,
  *                               318-320 (parse_header, block_ranges,
@@ -33,7 +38,7 @@
 extern "C" {
 #endif
 
-#define NVREC_ABI_VERSION 1
+#define NVREC_ABI_VERSION 2
 
 enum {
   NVREC_OK = 0,
@@ -127,6 +132,64 @@ typedef struct nvrec_lossmask_job {
  * Bit-exact with the reference receiver+codec. */
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream);
 
+/* Status codes written to nvrec_lossmask_job.status[0] (0 = ok):
+ *   1, 3 "header truncated"; 2 "inconsistent geometry in header";
+ *   4 "bitmap disagrees with present count"   (codec.UndecodableError)
+ *   10 invalid FrameKind                      (ValueError in parse_header)
+ *   5 grid_capacity too small                 (caller error)
+ * and, from nvrec_decode only:
+ *   6 "payload range is not whole RLE records";
+ *   7 "payload sample count disagrees with header"   (UndecodableError)
+ *   8 "P-frame decode requires a reference plane"    (ValueError)
+ *   9 plane_capacity too small                       (caller error) */
+
+/* One frame of codec.decode(enc, reference, zero_fill_ranges)
+ * (codec.py:260-321).  DEVICE pointers.  `mask` describes the header and
+ * the zero-filled ranges exactly as for nvrec_loss_mask and receives the
+ * grid / wire bits / status; mask.payload_received = len(enc.payload), the
+ * number of bytes at `payload` (the receiver's assembled body, zero chunks
+ * included, receiver.py:228-237).  The output plane is (h, w, c) u8 from
+ * the header; reference has the same shape and is required for P-frames
+ * (it may alias plane: in-place decode into a reference ring slot). */
+typedef struct nvrec_decode_job {
+  nvrec_lossmask_job mask;
+  const uint8_t* payload;
+  const uint8_t* reference;
+  uint8_t* plane;
+  int64_t plane_capacity;     /* bytes available at plane                     */
+  int32_t* scratch;           /* int32[mask.grid_capacity + 4] device scratch */
+} nvrec_decode_job;
+
+/* Batched decode: jobs is a DEVICE array; max_blocks >= every job's block
+ * count (h/block * w/block).  Bit-exact with the reference. */
+int nvrec_decode(const nvrec_decode_job* jobs, int32_t n_jobs, int32_t max_blocks, void* stream);
+
+/* Reed-Solomon erasure reconstruction (fec.rs_reconstruct, fec.py:144-163).
+ * nvrec_rs_plan runs on the HOST: given n data + r parity shards and
+ * present (u8[n+r], nonzero = received) it picks the first n present shards
+ * (sources, int32[n]; index < n = data shard, >= n = parity shard), lists
+ * the m missing data shards (missing, int32[>= r]) and writes the m x n GF(2^8)
+ * decode coefficients (coef, u8[>= r*n]).  Returns NVREC_E_INVALID with
+ * "only %d of %d required shards present" when fewer than n survive
+ * (UnrecoverableError).  m == 0 means the systematic fast path (no work). */
+int nvrec_rs_plan(int32_t n, int32_t r, const uint8_t* present, uint8_t* coef,
+                  int32_t* sources, int32_t* missing, int32_t* m_out);
+
+typedef struct nvrec_rs_job {
+  uint8_t* data;              /* n x shard_len: present data shards in place;
+                                 the m missing rows are written              */
+  const uint8_t* parity;      /* r x shard_len received parity shards        */
+  const uint8_t* coef;        /* m x n (nvrec_rs_plan)                       */
+  const int32_t* sources;     /* n                                            */
+  const int32_t* missing;     /* m                                            */
+  int32_t n, r, m, shard_len;
+} nvrec_rs_job;
+
+/* Batched GF(2^8) reconstruction of the missing data rows (DEVICE jobs
+ * array); max_shard_len >= every shard_len, max_coef >= every m*n. */
+int nvrec_rs_reconstruct(const nvrec_rs_job* jobs, int32_t n_jobs, int32_t max_shard_len,
+                         int32_t max_coef, int32_t aligned4, void* stream);
+
 /* Timeout / fault fallback on the GPU, bit-exact with the reference
  * recover_baseline_rgb / recover_baseline_depth (rgbdstream/recovery.py:94-196):
  * +-8 px SAD block match of every masked 16-px block against the most recent
@@ -146,7 +209,8 @@ enum {
   NVREC_STAGE_LOSSMASK = 0, NVREC_STAGE_MASKLIST = 1, NVREC_STAGE_COPY = 2,
   NVREC_STAGE_EMBED = 3, NVREC_STAGE_LNQKV = 4, NVREC_STAGE_ATTN_SIMT = 5,
   NVREC_STAGE_ATTN_TC = 6, NVREC_STAGE_TOKEN = 7, NVREC_STAGE_BASELINE = 8,
-  NVREC_NUM_STAGES = 9
+  NVREC_STAGE_DECODE = 9, NVREC_STAGE_RS = 10,
+  NVREC_NUM_STAGES = 11
 };
 int nvrec_profile_begin(void);
 int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages);

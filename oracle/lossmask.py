@@ -49,6 +49,8 @@ def parse_header(data: bytes) -> dict:
         raise UndecodableError("bitmap disagrees with present count")
     offsets = np.frombuffer(data, "<u4", n_present,
                             HDR_FIXED + bitmap_len).astype(np.int64)
+    if kind not in (0, 1):                 # _Header(FrameKind(kind), ...) (codec.py:200)
+        raise ValueError("%d is not a valid FrameKind" % kind)
     return dict(kind=kind, channels=ch, width=w, height=h, block=block,
                 quant=quant, payload_len=payload_len, present=present,
                 offsets=offsets, header_len=hdr_len)

@@ -28,9 +28,10 @@ EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_model_destroy", "nvrec_model_load", "nvrec_workspace_bytes",
            "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask",
            "nvrec_profile_begin", "nvrec_profile_end", "nvrec_baseline_workspace_bytes",
-           "nvrec_baseline_u8")
+           "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
-          "token", "baseline")
+          "token", "baseline", "decode", "rs")
+ABI_VERSION = 2
 
 
 class NativeError(RuntimeError):
@@ -52,6 +53,22 @@ class LossMaskJob(ctypes.Structure):
                 ("extra_ranges", ctypes.c_void_p), ("n_extra", ctypes.c_int32),
                 ("grid", ctypes.c_void_p), ("wire_bits", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("grid_capacity", ctypes.c_int32)]
+
+
+class DecodeJob(ctypes.Structure):
+    """``nvrec_decode_job``."""
+    _fields_ = [("mask", LossMaskJob), ("payload", ctypes.c_void_p),
+                ("reference", ctypes.c_void_p), ("plane", ctypes.c_void_p),
+                ("plane_capacity", ctypes.c_int64), ("scratch", ctypes.c_void_p)]
+
+
+class RsJob(ctypes.Structure):
+    """``nvrec_rs_job``."""
+    _fields_ = [("data", ctypes.c_void_p), ("parity", ctypes.c_void_p),
+                ("coef", ctypes.c_void_p), ("sources", ctypes.c_void_p),
+                ("missing", ctypes.c_void_p), ("n", ctypes.c_int32),
+                ("r", ctypes.c_int32), ("m", ctypes.c_int32),
+                ("shard_len", ctypes.c_int32)]
 
 
 _lib = None
@@ -88,11 +105,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_baseline_workspace_bytes.argtypes = [i32, i32, i32, i32]
         lib.nvrec_baseline_workspace_bytes.restype = i64
         lib.nvrec_baseline_u8.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp]
+        lib.nvrec_decode.argtypes = [vp, i32, i32, vp]
+        lib.nvrec_rs_plan.argtypes = [i32, i32, vp, vp, vp, vp, ctypes.POINTER(i32)]
+        lib.nvrec_rs_reconstruct.argtypes = [vp, i32, i32, i32, i32, vp]
         lib.nvrec_profile_end.argtypes = [ctypes.POINTER(ctypes.c_float),
                                           ctypes.POINTER(i32), i32]
         for name in EXPORTS:
             getattr(lib, name)
-        if lib.nvrec_abi_version() != 1:
+        if lib.nvrec_abi_version() != ABI_VERSION:
             raise RuntimeError("libnvrec_b200 ABI mismatch")
         _lib = lib
         return lib

@@ -589,6 +589,46 @@ int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream
   return 0;
 }
 
+int nvrec_decode(const nvrec_decode_job* jobs, int32_t n_jobs, int32_t max_blocks, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(NVREC_E_INVALID, "bad job array");
+  if (max_blocks < 1) return fail(NVREC_E_INVALID, "max_blocks must be >= 1");
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_DECODE, static_cast<cudaStream_t>(stream));
+    e = nvrec::launch_decode(jobs, n_jobs, max_blocks, static_cast<cudaStream_t>(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+  return 0;
+}
+
+int nvrec_rs_plan(int32_t n, int32_t r, const uint8_t* present, uint8_t* coef,
+                  int32_t* sources, int32_t* missing, int32_t* m_out) {
+  if (n < 1 || r < 0 || n + r > 255) return fail(NVREC_E_INVALID, "need n >= 1, r >= 0, n+r <= 255");
+  if (!present || !coef || !sources || !missing || !m_out)
+    return fail(NVREC_E_INVALID, "null pointer");
+  int have = 0;
+  for (int i = 0; i < n + r; ++i) have += present[i] != 0;
+  if (have < n) return fail(NVREC_E_INVALID, "only %d of %d required shards present", have, n);
+  const int rc = nvrec::rs_plan_host(n, r, present, coef, sources, missing, m_out);
+  if (rc == -2) return fail(NVREC_E_INVALID, "singular matrix");
+  if (rc) return fail(NVREC_E_INVALID, "rs plan failed");
+  return 0;
+}
+
+int nvrec_rs_reconstruct(const nvrec_rs_job* jobs, int32_t n_jobs, int32_t max_shard_len,
+                         int32_t max_coef, int32_t aligned4, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(NVREC_E_INVALID, "bad job array");
+  if (max_shard_len < 1 || max_coef < 0 || max_coef > 255 * 255)
+    return fail(NVREC_E_INVALID, "bad shard_len / coefficient bound");
+  cudaError_t e;
+  {
+    ProfScope ps(NVREC_STAGE_RS, static_cast<cudaStream_t>(stream));
+    e = nvrec::launch_rs(jobs, n_jobs, max_shard_len, max_coef, aligned4 != 0,
+                         static_cast<cudaStream_t>(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "rs launch");
+  return 0;
+}
 
 int64_t nvrec_baseline_workspace_bytes(int32_t b, int32_t h, int32_t w, int32_t c) {
   if (b < 1 || h < 16 || w < 16 || h % 16 || w % 16 || (c != 1 && c != 3))

@@ -104,6 +104,12 @@ cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
                             uint8_t* base, int* list, int* rank, int* count, int* bbox,
                             cudaStream_t s);
+cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_blocks,
+                          cudaStream_t s);
+int rs_plan_host(int n, int r, const uint8_t* present, uint8_t* coef, int32_t* sources,
+                 int32_t* missing, int32_t* m_out);
+cudaError_t launch_rs(const nvrec_rs_job* jobs, int n_jobs, int max_shard_len, int max_coef,
+                      bool word, cudaStream_t s);
 cudaError_t launch_masklist(const uint8_t* bits, int b, int nbytes, int ns, int* list,
                             int* rank, int* count, cudaStream_t s);
 

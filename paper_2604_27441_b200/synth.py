@@ -73,3 +73,146 @@ def p_frame_shards(rng, width, height, channels, shard_len, loss, present_ratio=
     for i in range(1, nd):
         received[i] = not loss()
     return header, nd, received, len(header) + payload_len
+
+
+# ---------------------------------------------------------------------------
+# Sender side of the codec + FEC, for building receiver workloads on the GPU
+# box (where the reference is absent).  Vectorised restatements of
+# rgbdstream codec.encode_i / encode_p (codec.py:212-247) with _blockify,
+# _rle_encode, _zigzag and _pack_header (codec.py:85-157), and fec.rs_encode
+# (fec.py:115-141).  tests/test_codec_oracle.py checks them byte-for-byte
+# against fixtures made by the reference encoder.
+
+KIND_I, KIND_P = 0, 1
+_HDR = "<BBHHBBIH"
+
+
+def _blockify(plane: np.ndarray, block: int) -> np.ndarray:
+    if plane.ndim == 2:
+        plane = plane[:, :, None]
+    h, w, c = plane.shape
+    a = plane.reshape(h // block, block, w // block, block, c).transpose(0, 2, 4, 1, 3)
+    return a.reshape((h // block) * (w // block), block * block * c)
+
+
+def _rle_encode(vals: np.ndarray, bs: int):
+    n = len(vals)
+    if n == 0:
+        return b"", np.zeros(0, np.int64)
+    change = np.flatnonzero(vals[1:] != vals[:-1]) + 1
+    starts = np.union1d(np.concatenate(([0], change)), np.arange(0, n, bs))
+    lengths = np.diff(np.concatenate((starts, [n])))
+    nchunks = (lengths + 254) // 255
+    total = int(nchunks.sum())
+    run_vals = np.repeat(vals[starts], nchunks)
+    run_lens = np.full(total, 255, np.int64)
+    last = np.cumsum(nchunks) - 1
+    run_lens[last] = lengths - (nchunks - 1) * 255
+    rec = np.empty((total, 3), np.uint8)
+    rec[:, 0] = run_lens
+    rec[:, 1] = run_vals & 0xFF
+    rec[:, 2] = run_vals >> 8
+    per_block = np.bincount(np.repeat(starts // bs, nchunks), minlength=n // bs)
+    offsets = np.concatenate(([0], np.cumsum(per_block[:-1]))) * 3
+    return rec.tobytes(), offsets
+
+
+def _header(kind, c, h, w, block, quant, payload_len, present, offsets) -> bytes:
+    return (struct.pack(_HDR, kind, c, w, h, block, quant, payload_len, int(present.sum()))
+            + np.packbits(present).tobytes() + np.asarray(offsets).astype("<u4").tobytes())
+
+
+def encode_i(plane: np.ndarray, quant: int = 4, block: int = 16):
+    """codec.py:212-222 -> (header, payload)."""
+    h, w = plane.shape[:2]
+    c = 1 if plane.ndim == 2 else plane.shape[2]
+    q = (plane.astype(np.uint16) + quant // 2) // quant
+    vals = _blockify(q, block).reshape(-1)
+    bs = block * block * c
+    payload, offsets = _rle_encode(vals, bs)
+    present = np.ones(len(vals) // bs, bool)
+    return _header(KIND_I, c, h, w, block, quant, len(payload), present, offsets), payload
+
+
+def encode_p(plane: np.ndarray, reference: np.ndarray, quant: int = 4, block: int = 16):
+    """codec.py:225-247 -> (header, payload)."""
+    h, w = plane.shape[:2]
+    c = 1 if plane.ndim == 2 else plane.shape[2]
+    d = plane.astype(np.int32) - reference.astype(np.int32)
+    qd = np.sign(d) * (np.abs(d) // quant)
+    blocks = _blockify(qd.astype(np.int16), block)
+    present = (blocks != 0).any(axis=1)
+    v = blocks[present].reshape(-1).astype(np.int16)
+    vals = ((v << 1) ^ (v >> 15)).astype(np.uint16)
+    payload, offsets = _rle_encode(vals, block * block * c)
+    return _header(KIND_P, c, h, w, block, quant, len(payload), present, offsets), payload
+
+
+def _gf_tables():
+    exp = np.zeros(512, np.uint8)
+    log = np.zeros(256, np.int32)
+    x = 1
+    for i in range(255):
+        exp[i], log[x] = x, i
+        x <<= 1
+        if x & 0x100:
+            x ^= 0x11D
+    exp[255:510] = exp[:255]
+    mul = np.zeros((256, 256), np.uint8)
+    a = np.arange(1, 256)
+    mul[1:, 1:] = exp[(log[a][:, None] + log[a][None, :]) % 255]
+    return mul
+
+
+_GF_MUL = None
+
+
+def _gf_inv(m: np.ndarray, mul) -> np.ndarray:
+    n = m.shape[0]
+    aug = np.concatenate((m.copy(), np.eye(n, dtype=np.uint8)), axis=1)
+    inv_of = np.zeros(256, np.uint8)
+    for a in range(1, 256):
+        inv_of[a] = np.flatnonzero(mul[a] == 1)[0]
+    for col in range(n):
+        piv = col + int(np.argmax(aug[col:, col] != 0))
+        if piv != col:
+            aug[[col, piv]] = aug[[piv, col]]
+        aug[col] = mul[inv_of[aug[col, col]], aug[col]]
+        f = aug[:, col].copy()
+        f[col] = 0
+        aug ^= mul[f[:, None], aug[col][None, :]]
+    return aug[:, n:]
+
+
+def rs_parity(data: bytes, n: int, r: int, shard_len: int) -> list[bytes]:
+    """fec.py:115-141: the r parity shards of ``data`` split into n shards."""
+    global _GF_MUL
+    if _GF_MUL is None:
+        _GF_MUL = _gf_tables()
+    mul = _GF_MUL
+    padded = np.frombuffer(data.ljust(n * shard_len, b"\x00"), np.uint8).reshape(n, shard_len)
+    if r == 0:
+        return []
+    points = np.arange(n + r, dtype=np.uint8)
+    vand = np.zeros((n + r, n), np.uint8)
+    vand[:, 0] = 1
+    for j in range(1, n):
+        vand[:, j] = mul[vand[:, j - 1], points]
+    top_inv = _gf_inv(vand[:n], mul)
+    gen = np.bitwise_xor.reduce(mul[vand[n:, :, None], top_inv[None, :, :]], axis=1)
+    parity = np.zeros((r, shard_len), np.uint8)
+    for i in range(r):
+        for j in range(n):
+            parity[i] ^= mul[gen[i, j]][padded[j]]
+    return [parity[i].tobytes() for i in range(r)]
+
+
+def i_frame_plan(encoded_len: int, payload_len: int, ratio: float = 0.5):
+    """fec.py:233-247 (REVO mode): (n, r, shard_len) of an I-frame."""
+    shard_len = payload_len
+    while True:
+        n = math.ceil(encoded_len / shard_len)
+        r = math.ceil(ratio * n)
+        if n + r <= 255:
+            return n, r, shard_len
+        shard_len *= 2
