@@ -4,25 +4,31 @@
 // time slice, head), non-causal, unmasked, head_dim 32, bf16 operands, fp32
 // scores / softmax / output.
 //
-// CTA = three 128-query tiles (round-robin on the tensor core) of one
-// (slice, head) sequence; 14 warps:
+// CTA = two 128-query tiles of one (slice, head) sequence; 10 warps:
 //   warps 4t..4t+3  softmax of query tile t (TMEM lanes 0-127, one row/thread)
-//   warp  12   TMA producer: Q tiles once, then K/V tiles through a 3-stage
+//   warp  8    TMA producer: Q tiles once, then K/V tiles through a 6-stage
 //              ring (K: 128 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x 2 x 128 B,
 //              SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
-//   warp  13   MMA issuer (one thread): S_t = Q_t K^T (M128 N128 K32, fp32 in
-//              TMEM), then PV_t = P_t V (M128 N32 K128, P read from TMEM where
-//              the softmax warps stored it as packed bf16 over S_t)
-// TMEM (512 columns): tile t owns S at [128t, 128t+128) and its output O at
-// [384+32t, 416+32t); P V accumulates into O across all key tiles.  Per key
-// tile j a softmax thread loads its S row (128 fp32), rescales O in TMEM only
-// when the running max of a row of its warp moved, computes the online-
-// softmax probabilities in base 2, and stores P (bf16) back over S.  MMAs of one thread execute in
-// issue order, so "S_t(j+1) after PV_tj" needs no extra fence, and the
-// commit after S_t(j+1) also certifies PV_tj.
+//   warp  9    MMA issuer (one thread)
+// TMEM (512 columns): every query tile owns two 128-column S buffers, so the
+// tensor core computes S(j+1) while the softmax warps work on S(j) -- the
+// softmax never waits for a QK^T round trip.  Key tile j of tile t:
+//   S(j)  = Q_t K_j^T            -> buf[t][j%2] (fp32, 128 columns)
+//   P(j)  = 2^(S*scale - m)      softmax warps, bf16 pairs over buf cols 0-63
+//   O'(j) = P(j) V_j             -> buf cols 64-95 (dead S columns; fresh
+//                                  accumulator, M128 N32 K128, P from TMEM)
+// and the softmax thread folds O'(j-1) into its register-resident output
+// O = O * 2^(m(j-2) - m(j-1)) + O'(j-1) right after its row max of S(j), then
+// releases the buffer for S(j+1).  No output rescaling round trips through
+// TMEM, no spin on the tensor core.
 //
-// The score rescale is the dominant cost: 128 MUFU ex2 per row per key tile
-// (the path is exp-bound).
+// Barriers per tile t: s_full[t][2] (S(j) ready, tcgen05.commit), p_full[t]
+// (P(j) stored, 128 arrivals), pv_full[t] (O'(j) ready, commit), o_read[t]
+// (O'(j) folded, 128 arrivals: buf[j%2] may take S(j+2)).
+//
+// The exponentials bind (head_dim 32 gives 128 MMA FLOP per exp, SURVEY.md
+// 8d): MUFU ex2 for most pairs, the FMA-pipe polynomial for one pair in
+// kPolyOf4 of each four.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,17 +44,17 @@ using namespace sm100;
 constexpr int kHd = 32;
 constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
-constexpr int kStages = 3;
-constexpr int kQT = 3;                                 // query tiles per CTA
+constexpr int kStages = 6;
+constexpr int kQT = 2;                                 // query tiles per CTA
 constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
+constexpr int kPolyOf4 = 1;                            // FMA-pipe exp2 pairs per 4
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
 constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
 constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
 constexpr uint32_t kIdescS = idesc_bf16(128, 128);
-// TMEM: S/P of tile t at [128t, 128t+128), its PV at [384 + 32t, 416 + 32t)
-constexpr uint32_t kColS = 128, kColPV = 384;
-static_assert(kQT * kColS <= kColPV && kColPV + 32 * kQT <= 512, "TMEM budget");
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
+constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buffer
+static_assert(kQT * 2 * kTileK <= 512, "TMEM budget");
 
 struct __align__(1024) Smem {
   uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
@@ -56,16 +62,18 @@ struct __align__(1024) Smem {
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[kQT], p_full[kQT];
+  uint64_t s_full[kQT][2], p_full[kQT], pv_full[kQT], o_read[kQT];
   uint32_t tmem_base;
 };
 
 struct TcArgs {
   float* ao;          // [b][nt][ns][64]
   const int* count;   // compact query count per stream, or null (= ns)
-  int nt, heads, ns, d;
+  int nt, heads, ns, d, seqs;
   float scale_log2;
 };
+
+__device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 * t + (j & 1)) * kTileK); }
 
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
@@ -75,14 +83,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   Smem& sm = *reinterpret_cast<Smem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seq = blockIdx.y;
+  // query-group-major order: every sequence's (short) last group runs last
+  const int seq = blockIdx.x % a.seqs;
+  const int group = blockIdx.x / a.seqs;
   const int b = seq / (a.nt * a.heads);
   const int nq = a.count ? a.count[b] : a.ns;
-  const int q0 = blockIdx.x * kQT * kTileQ;
+  const int q0 = group * kQT * kTileQ;
   if (q0 >= nq) return;                                   // uniform across the CTA
   const int nkv = (a.ns + kTileK - 1) / kTileK;
-  // query tiles with at least one live row (short compact lists use fewer)
-  const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);
+  const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
 
   const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
   if (warp == kProducer && lane == 0) {
@@ -92,8 +101,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_init(&sm.kv_empty[s], 1);
     }
     for (int t = 0; t < kQT; ++t) {
-      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.s_full[t][0], 1);
+      mbar_init(&sm.s_full[t][1], 1);
       mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.pv_full[t], 1);
+      mbar_init(&sm.o_read[t], 128);
     }
     fence_mbar_init();
     tma_prefetch(&tm_q);
@@ -128,40 +140,40 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       for (int t = 0; t < kQT; ++t)
         for (int kk = 0; kk < 2; ++kk)
           qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
-      auto issue_s = [&](int t, int s) {
-        const uint32_t kb = smem_u32(sm.k[s]);
-        for (int kk = 0; kk < 2; ++kk)
-          mma_ss(tmem + kColS * t, qdesc[t][kk], sdesc(kb + kk * 32, 512, kSwizzle64B),
-                 kIdescS, kk);
-        mma_commit(&sm.s_full[t]);
-      };
       mbar_wait(&sm.q_full, 0);
-      mbar_wait(&sm.kv_full[0], 0);
-      tc_fence_after();
-      for (int t = 0; t < ntq; ++t) issue_s(t, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % kStages;
-        const bool more = j + 1 < nkv;
-        const int s1 = (j + 1) % kStages;
-        for (int t = 0; t < ntq; ++t) {
-          mbar_wait(&sm.p_full[t], j & 1);
+      for (int j = 0; j <= nkv; ++j) {
+        if (j < nkv) {
+          // S_t(j) into buf[t][j%2] once O'(j-2) there has been folded
+          const int s = j % kStages;
+          mbar_wait(&sm.kv_full[s], (j / kStages) & 1);
           tc_fence_after();
-          const uint32_t vb = smem_u32(sm.v[s]);
-          for (int kk = 0; kk < 8; ++kk) {   // 16 keys per step: chunk kk/4, 32 B apart
-            const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
-            mma_ts(tmem + kColPV + 32 * t, tmem + kColS * t + kk * 8,
-                   sdesc(addr, 1024, kSwizzle128B), kIdescPV, (j | kk) != 0);
-          }
-          if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);   // K_j/V_j fully consumed
-          if (more) {
-            if (t == 0) {
-              mbar_wait(&sm.kv_full[s1], ((j + 1) / kStages) & 1);
+          const uint32_t kb = smem_u32(sm.k[s]);
+          for (int t = 0; t < ntq; ++t) {
+            if (j >= 2) {
+              mbar_wait(&sm.o_read[t], (j - 2) & 1);
               tc_fence_after();
             }
-            issue_s(t, s1);
-          } else {
-            mma_commit(&sm.s_full[t]);               // final: PV_t(last) done
+            for (int kk = 0; kk < 2; ++kk)
+              mma_ss(tmem + buf_col(t, j), qdesc[t][kk],
+                     sdesc(kb + kk * 32, 512, kSwizzle64B), kIdescS, kk);
+            mma_commit(&sm.s_full[t][j & 1]);
           }
+        }
+        if (j >= 1) {
+          // O'_t(j-1) = P_t(j-1) V_{j-1}: M128 N32, 16 keys per step
+          const int jp = j - 1, sp = jp % kStages;
+          const uint32_t vb = smem_u32(sm.v[sp]);
+          for (int t = 0; t < ntq; ++t) {
+            mbar_wait(&sm.p_full[t], jp & 1);
+            tc_fence_after();
+            const uint32_t bc = tmem + buf_col(t, jp);
+            for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
+              const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+              mma_ts(bc + kColOp, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+            }
+            mma_commit(&sm.pv_full[t]);
+          }
+          mma_commit(&sm.kv_empty[sp]);                 // K/V_{j-1} fully consumed
         }
       }
     }
@@ -171,48 +183,58 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quarter = warp & 3;            // TMEM lane quarter
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + kColS * t;
-    const uint32_t t_o = tmem + lane_off + kColPV + 32 * t;
-    float m = -INFINITY, l = 0.f;
+    float m = -INFINITY, l = 0.f, a_prev = 0.f;
+    float2 o2[kHd / 2];
+#pragma unroll
+    for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
     const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
+    const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
     for (int j = 0; j < jend; ++j) {
-      mbar_wait(&sm.s_full[t], j & 1);           // S_tj ready; also certifies PV_t(j-1)
+      const uint32_t t_s = tmem + lane_off + buf_col(t, j);
+      mbar_wait(&sm.s_full[t][j & 1], (j >> 1) & 1);
       tc_fence_after();
       const int valid = a.ns - j * kTileK;       // keys of this tile that exist
-      // pass 1: row max of the raw scores (32-column chunks keep registers low)
-      // (4 independent max chains: the dependent FMNMX chain was a stall source)
+      // pass 1: row max of the raw scores (two 32-column loads in flight)
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(t_s + 32 * ch, r);
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[64];
+        tmem_ld32(t_s + 64 * h, r);
+        tmem_ld32(t_s + 64 * h + 32, r + 32);
         tmem_wait_ld();
         if (valid >= kTileK) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
+          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            mx4[c & 3] = fmaxf(mx4[c & 3], 32 * ch + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+          for (int c = 0; c < 64; ++c)
+            mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
         }
       }
       const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float mn = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - mn);
-      // rescale the TMEM-resident output when any row of the warp moved its max
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+      // fold O'(j-1) (ready: issued when this thread finished P(j-1)), then
+      // hand its buffer back for S(j+1)
+      if (j > 0) {
+        mbar_wait(&sm.pv_full[t], (j - 1) & 1);
+        tc_fence_after();
         uint32_t ov[32];
-        tmem_ld32(t_o, ov);
+        tmem_ld32(tmem + lane_off + buf_col(t, j - 1) + kColOp, ov);
         tmem_wait_ld();
+        const float2 ap = make_float2(a_prev, a_prev);
 #pragma unroll
-        for (int e = 0; e < kHd; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-        tmem_st32(t_o, ov);
+        for (int e = 0; e < kHd / 2; ++e)
+          o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
+                                               __uint_as_float(ov[2 * e + 1])));
+        tc_fence_before();
+        mbar_arrive(&sm.o_read[t]);
       }
       // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
       // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
       // P pairs to columns [16ch, 16ch+16))
       float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-mn, -mn);
+      const float2 nm2 = make_float2(-mn, -mn);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32], pk[16];
@@ -227,8 +249,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 32; c += 2) {
           const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
                                  sc2, nm2);
-          // one pair in four on the FMA pipe, three on MUFU
-          const float2 p = ((c >> 1) & 3) == 3 ? exp2_poly2(v) : make_float2(ex2(v.x), ex2(v.y));
+          const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
+                                                     : make_float2(ex2(v.x), ex2(v.y));
           sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
           pk[c >> 1] = pack_bf16(p.x, p.y);
         }
@@ -236,27 +258,33 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
       l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
       m = mn;
+      a_prev = alpha;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
     }
-    if (t < ntq) {
-      mbar_wait(&sm.s_full[t], nkv & 1);         // final PV_t done
-      tc_fence_after();
-    }
-    uint32_t ov[32];
-    tmem_ld32(t_o, ov);
-    tmem_wait_ld();
     const int q = q0 + t * kTileQ + row;
-    if (t < ntq && q < nq) {
-      const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
-      const float inv = 1.f / l;
-      float4* dst = reinterpret_cast<float4*>(
-          a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
+    if (t < ntq) {
+      mbar_wait(&sm.pv_full[t], (nkv - 1) & 1);  // final O'
+      tc_fence_after();
+      uint32_t ov[32];
+      tmem_ld32(tmem + lane_off + buf_col(t, nkv - 1) + kColOp, ov);
+      tmem_wait_ld();
+      if (q < nq) {
+        const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
+        const float inv = 1.f / l;
+        float4* dst = reinterpret_cast<float4*>(
+            a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
 #pragma unroll
-      for (int e = 0; e < kHd; e += 4)
-        dst[e / 4] = make_float4(__uint_as_float(ov[e]) * inv, __uint_as_float(ov[e + 1]) * inv,
-                                 __uint_as_float(ov[e + 2]) * inv, __uint_as_float(ov[e + 3]) * inv);
+        for (int e = 0; e < kHd / 2; e += 2) {
+          const float2 x = ffma2(o2[e], make_float2(a_prev, a_prev),
+                                 make_float2(__uint_as_float(ov[2 * e]), __uint_as_float(ov[2 * e + 1])));
+          const float2 y = ffma2(o2[e + 1], make_float2(a_prev, a_prev),
+                                 make_float2(__uint_as_float(ov[2 * e + 2]),
+                                             __uint_as_float(ov[2 * e + 3])));
+          dst[e / 2] = make_float4(x.x * inv, x.y * inv, y.x * inv, y.y * inv);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -316,6 +344,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.heads = D.heads;
   ta.ns = A.ns;
   ta.d = D.d;
+  ta.seqs = seqs;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
@@ -323,7 +352,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr = true;
   }
-  dim3 grid(ceil_div(A.ns, kQT * kTileQ), seqs);
+  dim3 grid(ceil_div(A.ns, kQT * kTileQ) * seqs);
   attn_tc_kernel<<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
   return cudaGetLastError();
 }
