@@ -70,9 +70,10 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 template <int C>
 __global__ void __launch_bounds__(kThreads, 1)
 embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tcw) {
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   using S = EmbSmem<C>;
-  S& sm = *reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // pointer arithmetic (not integer casts) keeps the shared address space
+  S& sm = *reinterpret_cast<S*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_w = (a.nw + kTw - 1) / kTw;
   const int ih0 = (blockIdx.x / tiles_w) * kTh, iw0 = (blockIdx.x % tiles_w) * kTw;

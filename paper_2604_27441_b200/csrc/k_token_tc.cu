@@ -78,9 +78,9 @@ __device__ __forceinline__ void layernorm64(const float* x, float* y, const floa
 
 __global__ void __launch_bounds__(kThreads, 1)
 token_tc_kernel(TokenTcArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  TokSmem& sm =
-      *reinterpret_cast<TokSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // pointer arithmetic (not integer casts) keeps the shared address space
+  TokSmem& sm = *reinterpret_cast<TokSmem*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = warp >> 2, wq = warp & 3;        // tile slot, TMEM lane quarter
   const int nt = a.nt;
@@ -249,8 +249,8 @@ token_tc_kernel(TokenTcArgs a) {
       tmem_wait_ld();
 #pragma unroll
       for (int e = 0; e < 32; e += 2)
-        pk[e / 2] = pack_h2(gelu_erf(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e]),
-                            gelu_erf(__uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
+        pk[e / 2] = pack_h2(gelu_as(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e]),
+                            gelu_as(__uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
       tmem_st16(tbase + lane_off + 16 * c8, pk);   // columns [16 c8, 16 c8 + 16)
     }
     tmem_wait_st();
@@ -274,26 +274,42 @@ token_tc_kernel(TokenTcArgs a) {
     gemm_a(0, kOffQkvS, 192);
     int qrow = s;
     if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
+    // V^T stores in 4-byte pairs: lanes of adjacent positions (same slice)
+    // swap one value per dimension pair, so position pair (2i, 2i+1) of dims
+    // (e, e+1) goes out as two 32-bit stores instead of four 16-bit ones
+    const bool pairs = (ppw & 1) == 0;
+    const bool even = (jl & 1) == 0;
+    const int partner = even ? lane + nt : lane - nt;
+    const bool pair_ok = row_live && (s & ~1) < a.ns;
 #pragma unroll 1
     for (int c6 = 0; c6 < 6; ++c6) {
       uint32_t r[32];
       tmem_ld32(tbase + lane_off + 32 * c6, r);
       tmem_wait_ld();
-      if (!valid) continue;
       const int which = c6 >> 1, head = c6 & 1;
       const size_t seq = size_t(b * nt + it) * 2 + head;
       float v[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + P_[kPBQkvN + 32 * c6 + e];
       if (which < 2) {
-        if (which == 0 && qrow < 0) continue;
+        if (!valid || (which == 0 && qrow < 0)) continue;
         uint4* d4 = reinterpret_cast<uint4*>((which == 0 ? a.qh : a.kh) +
                                              (seq * a.ns_pad + (which == 0 ? qrow : s)) * 32);
 #pragma unroll
         for (int e = 0; e < 32; e += 8)
           d4[e / 8] = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
                                  pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
-      } else {
+      } else if (pairs) {
+        __nv_bfloat16* col = a.vth + seq * 32 * a.ns_pad + (s & ~1);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float mine = even ? v[e] : v[e + 1];
+          const float theirs = __shfl_sync(0xffffffffu, even ? v[e + 1] : v[e], partner);
+          const uint32_t w = even ? pack_bf16(mine, theirs) : pack_bf16(theirs, mine);
+          if (pair_ok)
+            *reinterpret_cast<uint32_t*>(col + size_t(even ? e : e + 1) * a.ns_pad) = w;
+        }
+      } else if (valid) {
         __nv_bfloat16* dst = a.vth + seq * 32 * a.ns_pad + s;
 #pragma unroll
         for (int e = 0; e < 32; ++e) dst[size_t(e) * a.ns_pad] = __float2bfloat16_rn(v[e]);
