@@ -121,7 +121,7 @@ void transpose_into(std::vector<float>& dst, const float* w, int out, int in) {
 }
 
 struct WorkspaceLayout {
-  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, total;
+  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, total;
 };
 
 WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
@@ -144,11 +144,12 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
     L.kh = take(seqrows * 2);
     L.vth = take(seqrows * 2);
     L.q = L.k = L.v = SIZE_MAX;
+    L.part = take(size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads * ns * 36 * 4);
   } else {
     L.q = take(seqrows * 4);
     L.k = take(seqrows * 4);
     L.v = take(seqrows * 4);
-    L.qh = L.kh = L.vth = SIZE_MAX;
+    L.qh = L.kh = L.vth = L.part = SIZE_MAX;
   }
   L.list = take(size_t(b) * ns * 4);
   L.rank = take(size_t(b) * ns * 4);
@@ -460,6 +461,7 @@ static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout
   A.list = at<int>(ws, L.list);
   A.rank = at<int>(ws, L.rank);
   A.count = at<int>(ws, L.count);
+  A.part = at<float>(ws, L.part);
   A.b = b;
   A.nh = h / m->D.p;
   A.nw = w / m->D.p;

@@ -77,8 +77,10 @@ struct Act {
   int* list;         // [b][ns] masked positions (ascending) or nullptr = dense
   int* rank;         // [b][ns] position -> row in list, -1 if absent
   int* count;        // [b] entries in list
+  float* part;       // bf16 path: key-split attention partials [split][seq][ns][36]
   int b, ns, nh, nw, ns_pad;
 };
+constexpr int kAttnMaxSplits = 3;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -29,6 +29,8 @@
 // The exponentials bind (head_dim 32 gives 128 MMA FLOP per exp, SURVEY.md
 // 8d): MUFU ex2 for most pairs, the FMA-pipe polynomial for one pair in
 // kPolyOf4 of each four.
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -62,39 +64,47 @@ struct __align__(1024) Smem {
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[kQT][2], p_full[kQT], pv_full[kQT], o_read[kQT];
+  uint64_t s_full[kQT][2], p_full[kQT], pv_full[kQT], o_read[kQT], done;
   uint32_t tmem_base;
 };
 
 struct TcArgs {
   float* ao;          // [b][nt][ns][64]
   const int* count;   // compact query count per stream, or null (= ns)
+  float* part;        // KV-split partials [split][seq][ns][kPart] or null
   int nt, heads, ns, d, seqs;
+  int splits;         // key-range splits (flash-decoding style) >= 1
+  int groups;         // query groups launched per (seq, split); CTAs loop
   float scale_log2;
 };
+constexpr int kPart = 36;                              // 32 output dims, m, l, 2 pad (16 B rows)
 
 __device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 * t + (j & 1)) * kTileK); }
 
+// kMulti: the CTA may loop over several query groups (pruned launches); the
+// dense instantiation runs exactly one group and keeps every counter at 0.
+template <bool kMulti>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // query-group-major order: every sequence's (short) last group runs last
   const int seq = blockIdx.x % a.seqs;
-  const int group = blockIdx.x / a.seqs;
+  const int split = (blockIdx.x / a.seqs) % a.splits;
+  const int group0 = blockIdx.x / (a.seqs * a.splits);
   const int b = seq / (a.nt * a.heads);
   const int nq = a.count ? a.count[b] : a.ns;
-  const int q0 = group * kQT * kTileQ;
-  if (q0 >= nq) return;                                   // uniform across the CTA
-  const int nkv = (a.ns + kTileK - 1) / kTileK;
-  const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
+  if (group0 * kQT * kTileQ >= nq) return;                // uniform across the CTA
+  const int nkv_all = (a.ns + kTileK - 1) / kTileK;
+  const int j0 = split * nkv_all / a.splits;              // this CTA's key tiles
+  const int nkv = (split + 1) * nkv_all / a.splits - j0;
 
   const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
   if (warp == kProducer && lane == 0) {
+    mbar_init(&sm.done, 1);
     mbar_init(&sm.q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.kv_full[s], 1);
@@ -118,178 +128,246 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == kProducer) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      mbar_expect_tx(&sm.q_full, ntq * kQBytes);
-      for (int t = 0; t < ntq; ++t)
-        tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % kStages;
-        mbar_wait(&sm.kv_empty[s], ((j / kStages) & 1) ^ 1);
-        mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
-        tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, j * kTileK, seq);
-        tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], j * kTileK, 0, seq);
-        tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], j * kTileK + 64, 0, seq);
-      }
-    }
-  } else if (warp == kMma) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      uint64_t qdesc[kQT][2];
-      for (int t = 0; t < kQT; ++t)
-        for (int kk = 0; kk < 2; ++kk)
-          qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
-      mbar_wait(&sm.q_full, 0);
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          // S_t(j) into buf[t][j%2] once O'(j-2) there has been folded
-          const int s = j % kStages;
-          mbar_wait(&sm.kv_full[s], (j / kStages) & 1);
-          tc_fence_after();
-          const uint32_t kb = smem_u32(sm.k[s]);
-          for (int t = 0; t < ntq; ++t) {
-            if (j >= 2) {
-              mbar_wait(&sm.o_read[t], (j - 2) & 1);
-              tc_fence_after();
-            }
-            for (int kk = 0; kk < 2; ++kk)
-              mma_ss(tmem + buf_col(t, j), qdesc[t][kk],
-                     sdesc(kb + kk * 32, 512, kSwizzle64B), kIdescS, kk);
-            mma_commit(&sm.s_full[t][j & 1]);
-          }
+  // Query groups group0, group0 + groups, ...: a pruned launch is sized for one
+  // group per sequence and loops when a stream has more masked patches.  The
+  // barriers are never re-initialised (a late tcgen05.commit arrival would
+  // land on a fresh barrier); every role keeps running use counts instead:
+  //   gkv    K/V tiles through the ring so far (stage, phase)
+  //   gs[t]  S tiles of query slot t so far (buffer, s_full/p_full/pv_full phase)
+  //   go[t]  O' folds of slot t so far (o_read phase)
+  //   gq     groups so far (q_full, done phase)
+  int gkv = 0, gq = 0, gs[kQT] = {}, go[kQT] = {};
+  for (int group = group0; group * kQT * kTileQ < nq; group += kMulti ? a.groups : nq) {
+    const int q0 = group * kQT * kTileQ;
+    const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
+
+    if (warp == kProducer) {
+      // ---------------------------------------------------------- TMA producer
+      if (lane == 0) {
+        mbar_expect_tx(&sm.q_full, ntq * kQBytes);
+        for (int t = 0; t < ntq; ++t)
+          tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
+        for (int j = 0; j < nkv; ++j) {
+          const int g = gkv + j, s = g % kStages;
+          mbar_wait(&sm.kv_empty[s], ((g / kStages) & 1) ^ 1);
+          mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
+          const int key0 = (j0 + j) * kTileK;
+          tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, key0, seq);
+          tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], key0, 0, seq);
+          tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], key0 + 64, 0, seq);
         }
-        if (j >= 1) {
-          // O'_t(j-1) = P_t(j-1) V_{j-1}: M128 N32, 16 keys per step
-          const int jp = j - 1, sp = jp % kStages;
-          const uint32_t vb = smem_u32(sm.v[sp]);
-          for (int t = 0; t < ntq; ++t) {
-            mbar_wait(&sm.p_full[t], jp & 1);
+      }
+    } else if (warp == kMma) {
+      // ---------------------------------------------------------- MMA issuer
+      if (lane == 0) {
+        uint64_t qdesc[kQT][2];
+        for (int t = 0; t < kQT; ++t)
+          for (int kk = 0; kk < 2; ++kk)
+            qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
+        mbar_wait(&sm.q_full, gq & 1);
+        for (int j = 0; j <= nkv; ++j) {
+          if (j < nkv) {
+            // S_t(j) into buf[t][j%2] once O'(j-2) there has been folded
+            const int g = gkv + j, s = g % kStages;
+            mbar_wait(&sm.kv_full[s], (g / kStages) & 1);
             tc_fence_after();
-            const uint32_t bc = tmem + buf_col(t, jp);
-            for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
-              const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
-              mma_ts(bc + kColOp, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+            const uint32_t kb = smem_u32(sm.k[s]);
+            for (int t = 0; t < ntq; ++t) {
+              if (j >= 2) {
+                mbar_wait(&sm.o_read[t], (go[t] + j - 2) & 1);
+                tc_fence_after();
+              }
+              for (int kk = 0; kk < 2; ++kk)
+                mma_ss(tmem + buf_col(t, gs[t] + j), qdesc[t][kk],
+                       sdesc(kb + kk * 32, 512, kSwizzle64B), kIdescS, kk);
+              mma_commit(&sm.s_full[t][(gs[t] + j) & 1]);
             }
-            mma_commit(&sm.pv_full[t]);
           }
-          mma_commit(&sm.kv_empty[sp]);                 // K/V_{j-1} fully consumed
+          if (j >= 1) {
+            // O'_t(j-1) = P_t(j-1) V_{j-1}: M128 N32, 16 keys per step
+            const int jp = j - 1, sp = (gkv + jp) % kStages;
+            const uint32_t vb = smem_u32(sm.v[sp]);
+            for (int t = 0; t < ntq; ++t) {
+              mbar_wait(&sm.p_full[t], (gs[t] + jp) & 1);
+              tc_fence_after();
+              const uint32_t bc = tmem + buf_col(t, gs[t] + jp);
+              for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
+                const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
+                mma_ts(bc + kColOp, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+              }
+              mma_commit(&sm.pv_full[t]);
+            }
+            mma_commit(&sm.kv_empty[sp]);               // K/V_{j-1} fully consumed
+          }
         }
+        mma_commit(&sm.done);             // the group's MMAs (Q reads) are complete
+        mbar_wait(&sm.done, gq & 1);
       }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax warps
-    const int t = warp >> 2;                 // query tile
-    const int quarter = warp & 3;            // TMEM lane quarter
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    float m = -INFINITY, l = 0.f, a_prev = 0.f;
-    float2 o2[kHd / 2];
+    } else {
+      // ---------------------------------------------------------- softmax warps
+      const int t = warp >> 2;                 // query tile
+      const int quarter = warp & 3;            // TMEM lane quarter
+      const int row = quarter * 32 + lane;
+      const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+      float m = -INFINITY, l = 0.f, a_prev = 0.f;
+      float2 o2[kHd / 2];
 #pragma unroll
-    for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
-    const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
-    const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
-    for (int j = 0; j < jend; ++j) {
-      const uint32_t t_s = tmem + lane_off + buf_col(t, j);
-      mbar_wait(&sm.s_full[t][j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      const int valid = a.ns - j * kTileK;       // keys of this tile that exist
-      // pass 1: row max of the raw scores (two 32-column loads in flight)
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
+      const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
+      const int gst = gs[t];
+      const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
+      for (int j = 0; j < jend; ++j) {
+        const int g = gst + j;
+        const uint32_t t_s = tmem + lane_off + buf_col(t, g);
+        mbar_wait(&sm.s_full[t][g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        const int valid = a.ns - (j0 + j) * kTileK;   // keys of this tile that exist
+        // pass 1: row max of the raw scores (two 32-column loads in flight)
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t r[64];
-        tmem_ld32(t_s + 64 * h, r);
-        tmem_ld32(t_s + 64 * h + 32, r + 32);
-        tmem_wait_ld();
-        if (valid >= kTileK) {
+        for (int h = 0; h < 2; ++h) {
+          uint32_t r[64];
+          tmem_ld32(t_s + 64 * h, r);
+          tmem_ld32(t_s + 64 * h + 32, r + 32);
+          tmem_wait_ld();
+          if (valid >= kTileK) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
-        } else {
+            for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
+          } else {
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
-            mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+            for (int c = 0; c < 64; ++c)
+              mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+          }
         }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        const float mn = fmaxf(m, mx * a.scale_log2);
+        const float alpha = ex2(m - mn);
+        // fold O'(j-1) (ready: issued when this thread finished P(j-1)), then
+        // hand its buffer back for S(j+1)
+        if (j > 0) {
+          mbar_wait(&sm.pv_full[t], (g - 1) & 1);
+          tc_fence_after();
+          uint32_t ov[32];
+          tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
+          tmem_wait_ld();
+          const float2 ap = make_float2(a_prev, a_prev);
+#pragma unroll
+          for (int e = 0; e < kHd / 2; ++e)
+            o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
+                                                 __uint_as_float(ov[2 * e + 1])));
+          tc_fence_before();
+          mbar_arrive(&sm.o_read[t]);
+        }
+        // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
+        // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and
+        // writes P pairs to columns [16ch, 16ch+16))
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 nm2 = make_float2(-mn, -mn);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t r[32], pk[16];
+          tmem_ld32(t_s + 32 * ch, r);
+          tmem_wait_ld();
+          if (valid < kTileK) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
+          }
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                   sc2, nm2);
+            const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
+                                                       : make_float2(ex2(v.x), ex2(v.y));
+            sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+            pk[c >> 1] = pack_bf16(p.x, p.y);
+          }
+          tmem_st16(t_s + 16 * ch, pk);
+        }
+        l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
+        m = mn;
+        a_prev = alpha;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
       }
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      const float mn = fmaxf(m, mx * a.scale_log2);
-      const float alpha = ex2(m - mn);
-      // fold O'(j-1) (ready: issued when this thread finished P(j-1)), then
-      // hand its buffer back for S(j+1)
-      if (j > 0) {
-        mbar_wait(&sm.pv_full[t], (j - 1) & 1);
+      const int q = q0 + t * kTileQ + row;
+      if (t < ntq) {
+        const int g = gst + nkv - 1;
+        mbar_wait(&sm.pv_full[t], g & 1);          // final O'
         tc_fence_after();
         uint32_t ov[32];
-        tmem_ld32(tmem + lane_off + buf_col(t, j - 1) + kColOp, ov);
+        tmem_ld32(tmem + lane_off + buf_col(t, g) + kColOp, ov);
         tmem_wait_ld();
-        const float2 ap = make_float2(a_prev, a_prev);
+        float o[kHd];
 #pragma unroll
-        for (int e = 0; e < kHd / 2; ++e)
-          o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
-                                               __uint_as_float(ov[2 * e + 1])));
-        tc_fence_before();
-        mbar_arrive(&sm.o_read[t]);
-      }
-      // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
-      // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and writes
-      // P pairs to columns [16ch, 16ch+16))
-      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      const float2 nm2 = make_float2(-mn, -mn);
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t r[32], pk[16];
-        tmem_ld32(t_s + 32 * ch, r);
-        tmem_wait_ld();
-        if (valid < kTileK) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
-        }
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
-                                 sc2, nm2);
-          const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
-                                                     : make_float2(ex2(v.x), ex2(v.y));
-          sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
-          pk[c >> 1] = pack_bf16(p.x, p.y);
-        }
-        tmem_st16(t_s + 16 * ch, pk);
-      }
-      l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
-      m = mn;
-      a_prev = alpha;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm.p_full[t]);
-    }
-    const int q = q0 + t * kTileQ + row;
-    if (t < ntq) {
-      mbar_wait(&sm.pv_full[t], (nkv - 1) & 1);  // final O'
-      tc_fence_after();
-      uint32_t ov[32];
-      tmem_ld32(tmem + lane_off + buf_col(t, nkv - 1) + kColOp, ov);
-      tmem_wait_ld();
-      if (q < nq) {
-        const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
-        const float inv = 1.f / l;
-        float4* dst = reinterpret_cast<float4*>(
-            a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
-#pragma unroll
-        for (int e = 0; e < kHd / 2; e += 2) {
+        for (int e = 0; e < kHd / 2; ++e) {
           const float2 x = ffma2(o2[e], make_float2(a_prev, a_prev),
                                  make_float2(__uint_as_float(ov[2 * e]), __uint_as_float(ov[2 * e + 1])));
-          const float2 y = ffma2(o2[e + 1], make_float2(a_prev, a_prev),
-                                 make_float2(__uint_as_float(ov[2 * e + 2]),
-                                             __uint_as_float(ov[2 * e + 3])));
-          dst[e / 2] = make_float4(x.x * inv, x.y * inv, y.x * inv, y.y * inv);
+          o[2 * e] = x.x;
+          o[2 * e + 1] = x.y;
+        }
+        if (q < nq && a.splits > 1) {
+          // unnormalised partial (O, m, l) of this key range; attn_combine merges
+          float* dst = a.part + ((size_t(split) * a.seqs + seq) * a.ns + q) * kPart;
+#pragma unroll
+          for (int e = 0; e < kHd; e += 4)
+            *reinterpret_cast<float4*>(dst + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          dst[32] = m;
+          dst[33] = l;
+        } else if (q < nq) {
+          const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
+          const float inv = 1.f / l;
+          float4* dst = reinterpret_cast<float4*>(
+              a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
+#pragma unroll
+          for (int e = 0; e < kHd; e += 4)
+            dst[e / 4] = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
         }
       }
     }
+    // next group: Q smem and TMEM are reused once everybody is done
+    if (!kMulti) break;
+    gkv += nkv;
+    ++gq;
+    for (int t = 0; t < ntq; ++t) {
+      gs[t] += nkv;
+      go[t] += nkv - 1;
+    }
+    tc_fence_before();
+    __syncwarp();
+    __syncthreads();
+    tc_fence_after();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// Merge the key-range partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
+// One thread per (row, output dim); 8 rows per 256-thread block, grid-stride.
+__global__ void __launch_bounds__(256)
+attn_combine_kernel(const float* __restrict__ part, float* __restrict__ ao,
+                    const int* __restrict__ count, int seqs, int splits, int nt, int heads,
+                    int ns, int d) {
+  const int seq = blockIdx.y;
+  const int b = seq / (nt * heads);
+  const int nq = count ? count[b] : ns;
+  const int it = (seq / heads) % nt, hh = seq % heads;
+  const int e = threadIdx.x & 31;
+  for (int q = blockIdx.x * 8 + (threadIdx.x >> 5); q < nq; q += gridDim.x * 8) {
+    float M = -INFINITY;
+    for (int sp = 0; sp < splits; ++sp)
+      M = fmaxf(M, __ldg(part + ((size_t(sp) * seqs + seq) * ns + q) * kPart + 32));
+    float o = 0.f, L = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+      const float* p = part + ((size_t(sp) * seqs + seq) * ns + q) * kPart;
+      const float w = ex2(__ldg(p + 32) - M);
+      L = fmaf(__ldg(p + 33), w, L);
+      o = fmaf(__ldg(p + e), w, o);
+    }
+    ao[(size_t(b * nt + it) * ns + q) * d + hh * kHd + e] = o / L;
+  }
 }
 
 // ---- host: tensor maps ---------------------------------------------------------
@@ -340,6 +418,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   TcArgs ta;
   ta.ao = A.ao;
   ta.count = count;
+  ta.part = A.part;
   ta.nt = D.nt;
   ta.heads = D.heads;
   ta.ns = A.ns;
@@ -347,13 +426,42 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.seqs = seqs;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
   const size_t smem = sizeof(Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  dim3 grid(ceil_div(A.ns, kQT * kTileQ) * seqs);
-  attn_tc_kernel<<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  // One CTA per SM (TMEM).  A pruned launch (compact masked-patch queries,
+  // count on the device) is sized for one query group per sequence and loops
+  // over further groups; a short grid splits the key range instead
+  // (flash-decoding partials merged by attn_combine_kernel) so every SM works.
+  const int nkv = ceil_div(A.ns, kTileK);
+  ta.groups = count ? 1 : ceil_div(A.ns, kQT * kTileQ);
+  int best = 1;
+  double best_t = 1e30;
+  for (int sp = 1; sp <= kAttnMaxSplits && sp <= nkv && A.part; ++sp) {
+    const int ctas = ta.groups * seqs * sp;
+    const double t = double(ceil_div(ctas, sms)) / sp + (sp > 1 ? 0.05 : 0.0);
+    if (t < best_t - 1e-9) { best_t = t; best = sp; }
+  }
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("NVREC_ATTN_SPLITS");      // debugging / experiments
+    force = e ? atoi(e) : -1;
+  }
+  if (force >= 1 && force <= kAttnMaxSplits && force <= nkv && A.part) best = force;
+  ta.splits = best;
+  dim3 grid(ta.groups * seqs * ta.splits);
+  if (count) attn_tc_kernel<true><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  else attn_tc_kernel<false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  if (ta.splits > 1) {
+    dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
+    attn_combine_kernel<<<cg, 256, 0, s>>>(A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,
+                                           A.ns, D.d);
+  }
   return cudaGetLastError();
 }
 
