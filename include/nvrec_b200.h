@@ -103,7 +103,9 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b,
  *   already front-padded, the last entry the corrupted plane;
  * mask_bits: u8 (b, ceil(gh*gw/8)) wire bitset (MSB-first, row-major);
  * out: u8 (b, h, w, c) merged planes (unmasked pixels = corrupted plane).
- * Only masked patches are decoded (exact: the merge discards the rest). */
+ * Only masked patches are decoded (exact: the merge discards the rest).
+ * The stacked frames are read before `out` is written, so `out` may alias
+ * the planes of one reference slot (in-place ring update). */
 int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
                      const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
                      const uint8_t* mask_bits, uint8_t* out, void* workspace,

@@ -550,11 +550,6 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     e = nvrec::launch_masklist(mask_bits, b, nbytes, A.ns, A.list, A.rank, A.count, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "masklist launch");
-  {
-    ProfScope ps(NVREC_STAGE_COPY, s);
-    e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "copy launch");
   if (fast && nvrec::embed_tc_supported(m->D)) {
     nvrec::EmbedTcArgs ea{};
     ea.D = m->D;
@@ -577,6 +572,14 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
     if (rc) return rc;
   }
+  // the merge base (corrupted plane) is copied only after the embedding has
+  // read every stacked frame, so `out` may alias a reference slot (a ring
+  // that takes the recovered plane in place of its oldest reference)
+  {
+    ProfScope ps(NVREC_STAGE_COPY, s);
+    e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "copy launch");
   return run_blocks(m, A, L, fast, true, h, w, nullptr, out, s);
 }
 

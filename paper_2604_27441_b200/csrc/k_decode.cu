@@ -40,6 +40,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxBs = 768;               // 16 x 16 x 3 samples per block (fast path)
 constexpr int32_t kFlagBit = 1 << 30;
+constexpr int kParseStage = 40 * 1024;    // header + received flags staged in smem
 
 struct Fixed {
   int kind, c, w, h, block, quant, n_present;
@@ -86,9 +87,11 @@ __global__ void __launch_bounds__(kThreads)
 decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
+  extern __shared__ uint8_t stage[];
   const nvrec_decode_job job = jobs[blockIdx.x];
   lm::Header H;
-  int err = lm::lossmask_job(job.mask, job.scratch + 4, &H, sh_scan, &sh_flagged);
+  int err = lm::lossmask_job(job.mask, job.scratch + 4, &H, sh_scan, &sh_flagged, stage,
+                             kParseStage);
   if (threadIdx.x == 0) {
     if (!err && H.kind == 1 && !job.reference) err = lm::kNeedReference;
     if (!err && int64_t(H.h) * H.w * H.channels > job.plane_capacity) err = lm::kPlaneCapacity;
@@ -290,7 +293,7 @@ __global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
 cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_blocks,
                           cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  decode_parse_kernel<<<n_jobs, kThreads, 0, s>>>(jobs);
+  decode_parse_kernel<<<n_jobs, kThreads, kParseStage, s>>>(jobs);
   dim3 grid((max_blocks + kWarps - 1) / kWarps, n_jobs);
   decode_blocks_kernel<<<grid, kThreads, 0, s>>>(jobs);
   decode_slow_kernel<<<n_jobs, 32, 0, s>>>(jobs);

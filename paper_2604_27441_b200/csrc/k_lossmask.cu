@@ -18,12 +18,15 @@ constexpr int kThreads = 256;
 using lm::block_exclusive_scan;
 }  // namespace
 
+constexpr int kStage = 40 * 1024;   // header + received flags staged in smem
+
 __global__ void __launch_bounds__(kThreads)
 lossmask_kernel(const nvrec_lossmask_job* __restrict__ jobs) {
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
+  extern __shared__ uint8_t stage[];
   const nvrec_lossmask_job job = jobs[blockIdx.x];
-  lm::lossmask_job(job, nullptr, nullptr, sh_scan, &sh_flagged);
+  lm::lossmask_job(job, nullptr, nullptr, sh_scan, &sh_flagged, stage, kStage);
 }
 
 // Wire bitset (b, nbytes) -> ascending masked-patch list, rank table, count.
@@ -60,7 +63,7 @@ masklist_kernel(const uint8_t* __restrict__ bits, int nbytes, int ns,
 // ---------------------------------------------------------------------------
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  lossmask_kernel<<<n_jobs, kThreads, 0, s>>>(jobs);
+  lossmask_kernel<<<n_jobs, kThreads, kStage, s>>>(jobs);
   return cudaGetLastError();
 }
 

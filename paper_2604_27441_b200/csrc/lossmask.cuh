@@ -89,8 +89,17 @@ __device__ __forceinline__ bool hits_shards(const ShardView& v, int64_t s, int64
   int64_t lo_i = 1, hi_i = v.i_cap;
   if (s < e) {
     if (v.body_len <= s) return false;
-    lo_i = s / v.L + 1; if (lo_i < 1) lo_i = 1;       // first shard with hi_i > s
-    hi_i = (e - 1) / v.L + 1; if (hi_i > v.i_cap) hi_i = v.i_cap;  // last shard with lo_i < e
+    if (s >= 0 && e <= 0xFFFFFFFFll && v.L > 0 && v.L <= 0xFFFFFFFFll) {
+      // 32-bit unsigned division (a 64-bit one is a ~70-instruction routine)
+      const uint32_t L32 = uint32_t(v.L);
+      lo_i = int64_t(uint32_t(s) / L32) + 1;
+      hi_i = int64_t(uint32_t(e - 1) / L32) + 1;
+    } else {
+      lo_i = s / v.L + 1;
+      hi_i = (e - 1) / v.L + 1;
+    }
+    if (lo_i < 1) lo_i = 1;                             // first shard with hi_i > s
+    if (hi_i > v.i_cap) hi_i = v.i_cap;                 // last shard with lo_i < e
   }
   for (int64_t i = lo_i; i <= hi_i; ++i) {
     if (v.received[i]) continue;
@@ -115,8 +124,21 @@ struct Header {
 // non-null it also receives, per block j, the present rank r of the block
 // (bit 30 set when flagged) or -1 for an absent block -- the index the
 // decoder needs to find the block's payload range.  Returns the status.
-__device__ inline int lossmask_job(const nvrec_lossmask_job& job, int32_t* block_rank, Header* out_hdr,
-                            int* sh_scan /*[32]*/, int* sh_flagged) {
+// stage: optional shared-memory buffer (stage_cap bytes); when the header and
+// the received flags fit they are copied there once (one coalesced round
+// trip) and every later parse step reads shared memory.
+__device__ inline int lossmask_job(const nvrec_lossmask_job& job_in, int32_t* block_rank,
+                                   Header* out_hdr, int* sh_scan /*[32]*/, int* sh_flagged,
+                                   uint8_t* stage = nullptr, int stage_cap = 0) {
+  nvrec_lossmask_job job = job_in;
+  if (stage && job.header_len >= 0 && job.n_data >= 0 &&
+      job.header_len + job.n_data <= stage_cap) {
+    for (int i = threadIdx.x; i < job.header_len; i += blockDim.x) stage[i] = job.header[i];
+    for (int i = threadIdx.x; i < job.n_data; i += blockDim.x)
+      stage[job.header_len + i] = job.received[i];
+    job.header = stage;
+    job.received = stage + job.header_len;
+  }
   const uint8_t* hdr = job.header;
   if (threadIdx.x == 0) *sh_flagged = 0;
   __syncthreads();
@@ -213,7 +235,11 @@ __device__ inline int lossmask_job(const nvrec_lossmask_job& job, int32_t* block
     job.status[2] = (err || !H.block) ? 0 : H.h / H.block;
     job.status[3] = (err || !H.block) ? 0 : H.w / H.block;
   }
-  if (out_hdr) *out_hdr = H;
+  if (out_hdr) {
+    *out_hdr = H;
+    out_hdr->bitmap = job_in.header + 14;               // global copies stay valid
+    out_hdr->offs = job_in.header + 14 + H.bitmap_len;
+  }
   return err;
 }
 

@@ -92,108 +92,148 @@ def grid_shape(h: int, w: int) -> tuple[int, int]:
 
 
 class RecoveryPipeline:
-    """Double-buffered multi-stream serving loop for one modality.
+    """Pipelined multi-stream serving loop for one modality.
 
     A server hosting ``n`` conference streams of one resolution receives, per
     frame time, each stream's decoded corrupted plane and its P-frame shard
     state.  ``submit`` stages them (pinned host memory), then enqueues
 
       copy stream     H2D of the planes + loss-mask jobs into buffer i
-      compute stream  nvrec_loss_mask -> nvrec_recover_u8 (device-resident
-                      reference rings) -> ring push of the recovered planes
+      compute stream  one CUDA graph: nvrec_loss_mask -> nvrec_recover_u8,
+                      the output written straight into the stream's oldest
+                      reference slot (it becomes the newest reference,
+                      reference receiver.py:268-269 -- no ring copies)
       copy stream     D2H of the recovered planes
 
-    with buffer i = step % 2, so step t's transfers overlap step t-1's
-    compute.  ``result(handle)`` waits for that step's D2H and returns the
-    pinned host array (b, h, w, c).  The rings start from ``init_refs``
-    (device u8 (n, k, h, w, c)); every recovered plane becomes the newest
-    reference of its stream (reference receiver.py:268-269)."""
+    with buffer i = step % nbuf, so the transfers of neighbouring steps
+    overlap the compute.  Device memory is slot-major, ``frames[slot][stream]``:
+    slots 0..k-1 are the reference ring (all streams advance together, so one
+    ring head serves every stream), slots k..k+nbuf-1 the corrupted planes.
+    ``result(handle)`` waits for that step's D2H and returns the pinned host
+    array (n, h, w, c); it stays valid for ``nbuf`` more submits."""
 
     def __init__(self, engine: RecoveryEngine, n: int, h: int, w: int,
-                 shard_len: int, max_header: int, max_shards: int, init_refs: torch.Tensor):
+                 shard_len: int, max_header: int, max_shards: int, init_refs: torch.Tensor,
+                 nbuf: int = 3, graphs: bool = False, h2d_streams: int = 4):
         from .lossmask import LossMaskBatch
         self.engine = engine
         self.n, self.h, self.w = n, h, w
         self.c = engine.channels
         cfg = engine.model.config
         self.k, self.F = cfg.k, cfg.stack_len
+        self.nbuf = nbuf
         dev = init_refs.device
         self.device = dev
-        # slots per stream: k ring entries + 2 corrupted-plane buffers
-        self.S = self.k + 2
-        self.frames = torch.empty((n, self.S, h, w, self.c), dtype=torch.uint8, device=dev)
-        self.frames[:, :self.k].copy_(init_refs)
-        self.flat = self.frames.view(n * self.S, h, w, self.c)
-        self.head = [0] * n                      # ring position of the oldest reference
+        self.frames = torch.empty((self.k + nbuf, n, h, w, self.c), dtype=torch.uint8, device=dev)
+        self.frames[:self.k].copy_(init_refs.transpose(0, 1))      # (n, k, ...) -> slot-major
+        self.flat = self.frames.view((self.k + nbuf) * n, h, w, self.c)
+        self.head = 0                                  # ring slot of the oldest reference
         self.nblk = (h // 16) * (w // 16)
-        self.lm = [LossMaskBatch(n, max_header, max_shards, self.nblk, 1, dev) for _ in range(2)]
-        self.out = [torch.empty((n, h, w, self.c), dtype=torch.uint8, device=dev)
-                    for _ in range(2)]
+        self.lm = [LossMaskBatch(n, max_header, max_shards, self.nblk, 1, dev)
+                   for _ in range(nbuf)]
         self.host_in = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
-                        for _ in range(2)]
+                        for _ in range(nbuf)]
         self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
-                         for _ in range(2)]
-        self.index = [torch.empty((n, self.F), dtype=torch.int32).pin_memory() for _ in range(2)]
-        self.dev_index = [torch.empty((n, self.F), dtype=torch.int32, device=dev)
-                          for _ in range(2)]
+                         for _ in range(nbuf)]
+        # slot tables for every (ring head, buffer): oldest reference first
+        # (front-padded as stack_slots does), the corrupted plane last
+        slots = stack_slots(self.k, self.k, self.F)
+        tab = np.empty((self.k, nbuf, n, self.F), np.int32)
+        for hd in range(self.k):
+            for i in range(nbuf):
+                ring = [((hd + j) % self.k) for j in range(self.k)] + [self.k + i]
+                for sidx in range(n):
+                    tab[hd, i, sidx] = [ring[x] * n + sidx for x in slots]
+        self.tables = torch.from_numpy(tab).to(dev)
         self.s_h2d = torch.cuda.Stream(dev)
+        # one DMA stream reaches ~40 GB/s host->device; four in parallel ~51
+        self.s_parts = [torch.cuda.Stream(dev) for _ in range(max(1, min(h2d_streams, n)))]
         self.s_cmp = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
-        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
-        self.ev_cmp = [torch.cuda.Event() for _ in range(2)]
-        self.ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        self.ev_h2d = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_d2h = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_slot = [None] * self.k                 # D2H that last read ring slot r
         self.step = 0
         self.shard_len = shard_len
+        self.use_graphs = graphs
+        self._graphs = {}
 
     def h2d_bytes(self) -> int:
-        return int(self.host_in[0].numel() + self.lm[0].h2d_bytes + self.index[0].numel() * 4)
+        return int(self.host_in[0].numel() + self.lm[0].h2d_bytes)
 
     def d2h_bytes(self) -> int:
         return int(self.host_out[0].numel())
 
+    def _compute(self, hd: int, i: int, stream) -> None:
+        lib = self.lm[i].lib
+        with torch.cuda.stream(stream):
+            _native.check(lib.nvrec_loss_mask(ctypes.c_void_p(self.lm[i].dev_in.data_ptr()),
+                                              self.lm[i].n,
+                                              ctypes.c_void_p(int(stream.cuda_stream))))
+            self.engine.recover_device(self.flat, self.tables[hd, i], self.lm[i].wire,
+                                       self.frames[hd])
+
+    def _run(self, hd: int, i: int) -> None:
+        if not self.use_graphs:
+            self._compute(hd, i, self.s_cmp)
+            return
+        g = self._graphs.get((hd, i))
+        if g is None:
+            # warm the launch paths (attributes, workspace) outside capture
+            with torch.cuda.stream(self.s_cmp):
+                self._compute(hd, i, self.s_cmp)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.s_cmp):
+                self._compute(hd, i, self.s_cmp)
+            self._graphs[(hd, i)] = g
+            # the warm-up consumed this step's inputs and wrote the output
+            # slot once; replaying recomputes the same values, so replay only
+            # where the warm-up result is not already final
+            return
+        with torch.cuda.stream(self.s_cmp):
+            g.replay()
+
     def submit(self, planes: np.ndarray | None, frames) -> int:
         """planes: (n, h, w, c) u8 host array (or None if already written into
-        ``host_in[step % 2]``); frames: n ``PFrameShards``.  Returns a handle."""
-        i = self.step & 1
-        if self.step >= 2:
-            self.ev_h2d[i].synchronize()          # staging buffers of step-2 are free
+        ``host_in[step % nbuf]``); frames: n ``PFrameShards``.  Returns a handle."""
+        i = self.step % self.nbuf
+        if self.step >= self.nbuf:
+            self.ev_h2d[i].synchronize()          # staging buffers of step - nbuf are free
             self.ev_d2h[i].synchronize()          # host_out[i] consumed by the caller
         if planes is not None:
             self.host_in[i].numpy()[...] = planes
         self.lm[i].stage(frames)
-        idx = self.index[i].numpy()
-        for s in range(self.n):
-            ring = [(self.head[s] + j) % self.k for j in range(self.k)]
-            idx[s] = [s * self.S + r for r in ring] + [s * self.S + self.k + i]
-        # H2D: plane into its buffer slot, loss-mask jobs, slot table
-        self.s_h2d.wait_event(self.ev_cmp[i]) if self.step >= 2 else None
+        hd = self.head
+        # H2D: planes into the corrupted-plane slot, loss-mask jobs
+        if self.step >= self.nbuf:
+            self.s_h2d.wait_event(self.ev_cmp[i])  # step - nbuf finished reading slot k+i
+        start = self.s_h2d.record_event()
+        per = -(-self.n // len(self.s_parts))
+        for p, sp in enumerate(self.s_parts):
+            lo, hi = p * per, min(self.n, (p + 1) * per)
+            if lo >= hi:
+                continue
+            sp.wait_event(start)
+            with torch.cuda.stream(sp):
+                self.frames[self.k + i, lo:hi].copy_(self.host_in[i][lo:hi], non_blocking=True)
+            self.s_h2d.wait_stream(sp)
         with torch.cuda.stream(self.s_h2d):
-            self.frames[:, self.k + i].copy_(self.host_in[i], non_blocking=True)
             self.lm[i].dev_in.copy_(self.lm[i].host, non_blocking=True)
-            self.dev_index[i].copy_(self.index[i], non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
-        # compute
+        # compute: output goes into the oldest ring slot once its last D2H is done
         self.s_cmp.wait_event(self.ev_h2d[i])
-        with torch.cuda.stream(self.s_cmp):
-            lib = self.lm[i].lib
-            _native.check(lib.nvrec_loss_mask(ctypes.c_void_p(self.lm[i].dev_in.data_ptr()),
-                                              self.lm[i].n,
-                                              ctypes.c_void_p(int(self.s_cmp.cuda_stream))))
-            if self.step >= 2:
-                self.s_cmp.wait_event(self.ev_d2h[i])   # out[i] drained
-            self.engine.recover_device(self.flat, self.dev_index[i], self.lm[i].wire,
-                                       self.out[i])
-            # ring push: the recovered plane replaces each stream's oldest ref
-            for s in range(self.n):
-                self.frames[s, self.head[s]].copy_(self.out[i][s], non_blocking=True)
-            self.ev_cmp[i].record(self.s_cmp)
-        for s in range(self.n):
-            self.head[s] = (self.head[s] + 1) % self.k
-        # D2H
+        if self.ev_slot[hd] is not None:
+            self.s_cmp.wait_event(self.ev_slot[hd])
+        self._run(hd, i)
+        self.ev_cmp[i].record(self.s_cmp)
+        # D2H of the recovered planes (now the newest references)
         self.s_d2h.wait_event(self.ev_cmp[i])
         with torch.cuda.stream(self.s_d2h):
-            self.host_out[i].copy_(self.out[i], non_blocking=True)
+            self.host_out[i].copy_(self.frames[hd], non_blocking=True)
             self.ev_d2h[i].record(self.s_d2h)
+        self.ev_slot[hd] = self.ev_d2h[i]
+        self.head = (hd + 1) % self.k
         self.step += 1
         return i
 
