@@ -209,6 +209,80 @@ class ModalityWork:
         return int(self.host_out.numel())
 
 
+class ReceiverWork:
+    """S streams of one modality as the receiver sees them: per frame time a
+    codec P-frame (synthetic talking-motion content, encoded by the sender
+    restatement in synth.py) whose body shards went through the GE channel;
+    decoded + recovered on the GPU by ReceiverPipeline."""
+
+    def __init__(self, name, c, L, stream_ids, device, engine, n_frames=6):
+        from paper_2604_27441_b200 import synth
+        from paper_2604_27441_b200.receiver import ReceiverPipeline
+        from paper_2604_27441_b200.synth import GilbertElliott
+        self.name, self.c, self.S = name, c, len(stream_ids)
+        seqs, init = [], []
+        max_hdr = max_body = max_nd = 0
+        for s, sid in enumerate(stream_ids):
+            clip = synth.talking_clip(n_frames + 1, W, H, c, seed=sid * 7 + c)
+            seq = []
+            ge = GilbertElliott(seed=sid + 31 * c)
+            prev = clip[0]                        # sender reference (lossless side)
+            for f in clip[1:]:
+                hp, pp = synth.encode_p(f, prev)
+                nd = synth.n_data_shards(len(pp), L)
+                recv = np.ones(nd, bool)
+                for i in range(1, nd):
+                    recv[i] = not ge.drop()
+                if recv.all():
+                    recv[1 + (s % max(1, nd - 1))] = False
+                seq.append((hp, synth.receiver_body(pp, L, recv), recv, L))
+                max_hdr, max_body, max_nd = max(max_hdr, len(hp)), max(max_body, len(pp)), \
+                    max(max_nd, nd)
+                prev = f
+            seqs.append(seq)
+            init.append(np.stack([clip[0]] * 5).reshape(5, H, W, c))
+        self.seqs = seqs
+        self.n_frames = n_frames
+        init_t = torch.from_numpy(np.stack(init)).to(device)
+        self.pipe = ReceiverPipeline(engine, self.S, H, W, init_t, max_hdr + 16, max_body + 16,
+                                     max_nd + 1)
+        self.t = 0
+
+    def submit(self):
+        j = self.t % self.n_frames
+        self.t += 1
+        return self.pipe.submit([seq[j] for seq in self.seqs])
+
+
+def timed_receiver(rworks, steps, dist_on):
+    """Receiver back end end to end: compressed P-frames in (pinned H2D),
+    GPU decode + loss mask + recovery, displayable planes out (D2H)."""
+    main = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    if dist_on:
+        torch.distributed.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(main)
+    for rw in rworks:
+        rw.pipe.s_h2d.wait_event(t0)
+    h2d = 0
+    for _ in range(steps):
+        for rw in rworks:
+            hnd = rw.submit()
+            h2d += rw.pipe.h2d_bytes(hnd)
+    for rw in rworks:
+        main.wait_stream(rw.pipe.s_d2h)
+    t1.record(main)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if dist_on:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, h2d / steps
+
+
 def timed_pipeline(works, steps, dist_on):
     """End-to-end serving throughput: every step submits each stream's new
     corrupted plane + loss-mask job from pinned host memory and returns the
@@ -394,6 +468,13 @@ def main():
     ms_e2e = timed_pipeline(works, args.steps, dist_on)
     ms_e2e_serial = timed(works, streams, "e2e_step", max(3, args.steps // 4), dist_on)
     ms_proto = timed(works, streams, "protocol_step", max(3, args.steps // 4), dist_on)
+    # receiver back end: compressed P-frames in, decode + recovery on the GPU
+    rworks = [ReceiverWork(n, c, L, mine, device, wk.engine) for (n, c, L), wk in zip(MODS, works)]
+    for _ in range(4):
+        for rw in rworks:
+            rw.submit()
+    torch.cuda.synchronize()
+    ms_recv, recv_h2d = timed_receiver(rworks, args.steps, dist_on)
     # per-stage device times: separate pass, both modalities serialised on ONE
     # stream so event brackets are not inflated by the concurrent modality
     torch.cuda.synchronize()
@@ -484,6 +565,16 @@ def main():
                          "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works),
                          "path": "reference wire-protocol payload: all k references re-sent "
                                  "per request (recovery.py:219-227)"},
+        "e2e_receiver": {"value": S * world * args.steps / (ms_recv / 1000.0), "unit": "frames/s",
+                         "h2d_bytes_per_step": int(recv_h2d),
+                         "d2h_bytes_per_step": sum(rw.pipe.d2h_bytes() for rw in rworks),
+                         "path": "ReceiverPipeline: per step each stream's received P-frame "
+                                 "(codec header + assembled body with zero-filled lost "
+                                 "shards, receiver.py:222-237) H2D, nvrec_decode (zero-fill "
+                                 "decode + loss mask, codec.py:260-321) against the newest "
+                                 "ring plane, nvrec_recover_u8 into the ring, D2H of the "
+                                 "displayable planes; synthetic talking-motion 720p content "
+                                 "encoded by the synth.py sender, GE channel loss"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "p50_latency_ms": statistics.median(lat),
         "p99_latency_ms": float(np.percentile(lat, 99)),

@@ -1,0 +1,140 @@
+"""Device-resident receiver back end: P-frame decode + recovery on the GPU.
+
+Replaces, for ``n`` streams of one modality, the tail of the reference
+receiver's P-frame finalisation (rgbdstream/receiver.py:211-274):
+
+  body assembly      received body shards + zero chunks (receiver.py:228-237)
+                     -- done by the caller on the host, it is what arrived
+  codec.decode       zero-fill decode against the stream's newest displayable
+                     plane (``self.refs[modality]``, receiver.py:244-247) and
+                     the corruption mask (codec.py:260-321) -> nvrec_decode
+  backend(req)       recovery with the k-frame ring (receiver.py:260-264)
+                     -> nvrec_recover_u8, output straight into the ring
+  ring push          the recovered plane replaces the oldest reference
+                     (receiver.py:268-269), in place
+
+Per frame time only the compressed bytes travel host -> device (codec header
++ assembled body, ~60-200 KB at 720p instead of a 2.8 MB plane), and the
+displayable plane comes back.  Decode errors (``UndecodableError`` in the
+reference, i.e. LOST_FRAME) are reported per stream by ``result``; a lost
+frame's slot then holds a partially decoded plane, exactly as the caller's
+fallback policy decides what to display.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .codec import DecodeBatch, DecodeItem, raise_status
+from .recovery import RecoveryEngine, stack_slots
+
+
+class ReceiverPipeline:
+    """Pipelined receive -> decode -> recover loop for ``n`` streams.
+
+    ``submit(frames)`` takes one received P-frame per stream as
+    (header bytes, assembled body bytes, received-shard flags, shard_len) and
+    returns a handle; ``result(handle)`` returns the displayable planes
+    (n, h, w, c) in pinned host memory and the per-stream decode status."""
+
+    def __init__(self, engine: RecoveryEngine, n: int, h: int, w: int, init_refs: torch.Tensor,
+                 max_header: int, max_payload: int, max_shards: int, nbuf: int = 3):
+        self.engine = engine
+        self.n, self.h, self.w = n, h, w
+        self.c = engine.channels
+        cfg = engine.model.config
+        self.k, self.F = cfg.k, cfg.stack_len
+        self.nbuf = nbuf
+        dev = init_refs.device
+        self.device = dev
+        self.frames = torch.empty((self.k + nbuf, n, h, w, self.c), dtype=torch.uint8, device=dev)
+        self.frames[:self.k].copy_(init_refs.transpose(0, 1))      # (n, k, ...) -> slot-major
+        self.flat = self.frames.view((self.k + nbuf) * n, h, w, self.c)
+        self.head = 0                                   # ring slot of the oldest reference
+        nblk = (h // 16) * (w // 16)
+        self.dec = [DecodeBatch(n, max_header, max_payload, nblk, max_shards=max_shards,
+                                max_ranges=1, device=dev) for _ in range(nbuf)]
+        self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
+                         for _ in range(nbuf)]
+        slots = stack_slots(self.k, self.k, self.F)
+        tab = np.empty((self.k, nbuf, n, self.F), np.int32)
+        for hd in range(self.k):
+            for i in range(nbuf):
+                ring = [((hd + j) % self.k) for j in range(self.k)] + [self.k + i]
+                for s in range(n):
+                    tab[hd, i, s] = [ring[x] * n + s for x in slots]
+        self.tables = torch.from_numpy(tab).to(dev)
+        self.s_h2d = torch.cuda.Stream(dev)
+        self.s_cmp = torch.cuda.Stream(dev)
+        self.s_d2h = torch.cuda.Stream(dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_d2h = [torch.cuda.Event() for _ in range(nbuf)]
+        self.ev_slot = [None] * self.k
+        self.step = 0
+        self.bytes_in = [0] * nbuf
+
+    def h2d_bytes(self, handle: int | None = None) -> int:
+        """Compressed bytes shipped for one step (headers + bodies + descriptors)."""
+        return int(self.bytes_in[self.step % self.nbuf if handle is None else handle])
+
+    def d2h_bytes(self) -> int:
+        return int(self.host_out[0].numel())
+
+    def submit(self, frames) -> int:
+        """frames: n tuples (header, body, received flags, shard_len)."""
+        i = self.step % self.nbuf
+        if self.step >= self.nbuf:
+            self.ev_h2d[i].synchronize()
+            self.ev_d2h[i].synchronize()
+        hd = self.head
+        newest = (hd - 1) % self.k
+        items = []
+        for s, (header, body, received, shard_len) in enumerate(frames):
+            items.append(DecodeItem(header, body, self.frames[self.k + i, s],
+                                    self.frames[newest, s], n_data=len(received),
+                                    received=received, shard_len=shard_len,
+                                    body_len=len(body)))
+        dec = self.dec[i]
+        dec.stage(items)
+        self.bytes_in[i] = dec.o_pay + sum(len(f[1]) for f in frames)
+        if self.step >= self.nbuf:
+            self.s_h2d.wait_event(self.ev_cmp[i])       # staging buffer of step - nbuf read
+        with torch.cuda.stream(self.s_h2d):
+            # descriptors + headers + bodies: copy only the used prefix of each
+            # job's region (the staging layout is job-strided)
+            dec.dev_in[:dec.o_pay].copy_(dec.host[:dec.o_pay], non_blocking=True)
+            for j, f in enumerate(frames):
+                lo = dec.o_pay + j * dec.max_payload
+                dec.dev_in[lo:lo + len(f[1])].copy_(dec.host[lo:lo + len(f[1])],
+                                                    non_blocking=True)
+            lo, hi = dec.o_recv, dec.in_bytes
+            dec.dev_in[lo:hi].copy_(dec.host[lo:hi], non_blocking=True)
+            self.ev_h2d[i].record(self.s_h2d)
+        self.s_cmp.wait_event(self.ev_h2d[i])
+        if self.ev_slot[hd] is not None:
+            self.s_cmp.wait_event(self.ev_slot[hd])
+        with torch.cuda.stream(self.s_cmp):
+            dec.launch(self.s_cmp, copy=False)
+            self.engine.recover_device(self.flat, self.tables[hd, i], dec.wire, self.frames[hd])
+            self.ev_cmp[i].record(self.s_cmp)
+        self.s_d2h.wait_event(self.ev_cmp[i])
+        with torch.cuda.stream(self.s_d2h):
+            self.host_out[i].copy_(self.frames[hd], non_blocking=True)
+            self.ev_d2h[i].record(self.s_d2h)
+        self.ev_slot[hd] = self.ev_d2h[i]
+        self.head = (hd + 1) % self.k
+        self.step += 1
+        return i
+
+    def result(self, handle: int, check: bool = True):
+        """(planes (n, h, w, c), per-stream decode status codes).  With
+        ``check`` the first failing stream raises like ``codec.decode``."""
+        self.ev_d2h[handle].synchronize()
+        st = self.dec[handle].status[:self.n, 0].cpu().numpy()
+        if check:
+            for s in range(self.n):
+                raise_status(int(st[s]), self.dec[handle].headers[s])
+        return self.host_out[handle].numpy(), st

@@ -101,3 +101,54 @@ def test_recovery_pipeline_matches_sequential_engine():
             got = pipe.result(handles[step - 1])
             assert np.array_equal(got, expected[step - 1])
     assert np.array_equal(pipe.result(handles[-1]), expected[-1])
+
+
+def test_receiver_pipeline_matches_reference_receiver_chain():
+    """GPU receiver (decode -> mask -> recover -> in-place ring) == the
+    reference receiver's chain restated with the oracle decode
+    (codec.py:260-321, receiver.py:222-269) and per-request engine calls."""
+    from paper_2604_27441_b200 import synth
+    from paper_2604_27441_b200.receiver import ReceiverPipeline
+    from paper_2604_27441_b200.recovery import RecoveryEngine
+    from oracle import codec as oc
+    ck, _ = _ck(3, 504)
+    eng = RecoveryEngine(ck.build_model(), "fast")
+    n, h, w, c, k, L = 2, 64, 96, 3, 5, 256
+    rng = np.random.default_rng(9)
+    clips = [synth.talking_clip(12, w, h, c, seed=40 + s, motion_fraction=0.3) for s in range(n)]
+    # the sender encodes against its own clean reconstruction
+    enc, refs, disp = [], [], []
+    for s in range(n):
+        hi, pi = synth.encode_i(clips[s][0])
+        rec, _ = oc.decode(hi, pi)
+        seq = []
+        for f in clips[s][1:]:
+            hp, pp = synth.encode_p(f, rec)
+            rec, _ = oc.decode(hp, pp, rec)
+            seq.append((hp, pp))
+        enc.append(seq)
+        refs.append([clips[s][0]] * k)
+        disp.append(clips[s][0])
+    init = torch.from_numpy(np.stack([np.stack(r) for r in refs])).cuda()
+    pipe = ReceiverPipeline(eng, n, h, w, init, 4096, 1 << 16, 64)
+    for step in range(6):
+        frames, expected = [], []
+        for s in range(n):
+            hp, pp = enc[s][step]
+            nd = synth.n_data_shards(len(pp), L)
+            recv = np.ones(nd, bool)
+            recv[1:] = rng.random(nd - 1) >= 0.3
+            body = synth.receiver_body(pp, L, recv)
+            frames.append((hp, body, recv, L))
+            shards = {i: pp[(i - 1) * L:i * L] for i in range(1, nd) if recv[i]}
+            b2, zf = oc.finalize_p_body(nd, shards, L, len(pp))
+            assert b2 == body
+            plane, grid = oc.decode(hp, b2, disp[s], zf)
+            out = eng.recover(plane, grid, refs[s]) if grid.any() else plane
+            refs[s] = refs[s][1:] + [out]
+            disp[s] = out
+            expected.append(out)
+        hnd = pipe.submit(frames)
+        got, st = pipe.result(hnd)
+        assert not st.any()
+        assert np.array_equal(got, np.stack(expected))
