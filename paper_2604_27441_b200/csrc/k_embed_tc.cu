@@ -34,25 +34,32 @@ using namespace sm100;
 
 constexpr int kRows = 128;
 constexpr int kTh = 8, kTw = 16;   // patch rectangle per CTA
-constexpr int kNst = 3;            // A/W (MMA operand) ring depth
-constexpr int kNu8 = 6;            // raw-pixel TMA ring depth (prefetch distance)
 constexpr int kThreads = 192;
 
+// RGB: two CTAs per SM (<= ~113 KB of shared memory each), so one CTA's
+// epilogue and qkv GEMM overlap the other's pixel stream; the qkv weights
+// reuse the A ring and the LN output reuses the raw-pixel ring once the K loop
+// is done.  Depth (c = 1) has small stages: deeper rings, same sharing.
 template <int C>
 struct __align__(128) EmbSmem {
+  static constexpr int kNst = C == 3 ? 2 : 3;                // A/W (MMA operand) ring
+  static constexpr int kNu8 = C == 3 ? 3 : 6;                // raw-pixel TMA ring
   static constexpr uint32_t kU8 = kTh * 2 * kTw * 16 * C;   // raw pixels per stage
   static constexpr uint32_t kA = kRows * 32 * C * 2;        // fp16 A per stage
   static constexpr uint32_t kW = 64 * 32 * C * 2;           // fp16 W per stage
-  uint8_t a[kNst][kA];
+  static constexpr uint32_t kQkvW = 192 * 64 * 2, kA2 = kRows * 64 * 2;
+  static constexpr uint32_t kARegion = kNst * kA > kQkvW ? kNst * kA : kQkvW;
+  static constexpr uint32_t kURegion = kNu8 * kU8 > kA2 ? kNu8 * kU8 : kA2;
+  uint8_t a_raw[kARegion];        // A ring, then: qkv weights [192 x 64] fp16
   uint8_t w[kNst][kW];
-  uint8_t u8[kNu8][kU8];
-  uint8_t a2[kRows * 64 * 2];
-  uint8_t wq[192 * 64 * 2];
+  uint8_t u8_raw[kURegion];       // pixel ring, then: LN output (A2) [128 x 64] fp16
   float par[64 * 5 + 192];        // bias | time_pos[it] | wmsum | ln_w | ln_b | qkv_b
   uint64_t u8_full[kNu8], u8_empty[kNu8], w_full[kNst], aready[kNst], empty[kNst];
   uint64_t acc_full, wq_full, a2_ready, qkv_full;
   uint32_t tmem_base;
   int slot[16];
+  __device__ uint8_t* a(int i) { return a_raw + i * kA; }
+  __device__ uint8_t* u8(int i) { return u8_raw + i * kU8; }
 };
 
 __device__ __forceinline__ uint32_t u8x2_to_h2(uint32_t w, uint32_t sel) {
@@ -81,11 +88,11 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   const int T = a.D.T, nst = T * 8;
 
   if (warp == 4 && lane == 0) {
-    for (int i = 0; i < kNu8; ++i) {
+    for (int i = 0; i < S::kNu8; ++i) {
       mbar_init(&sm.u8_full[i], 1);
       mbar_init(&sm.u8_empty[i], 128);
     }
-    for (int i = 0; i < kNst; ++i) {
+    for (int i = 0; i < S::kNst; ++i) {
       mbar_init(&sm.w_full[i], 1);
       mbar_init(&sm.aready[i], 128);
       mbar_init(&sm.empty[i], 1);
@@ -115,36 +122,38 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   if (warp == 4) {
     // ---------------------------------------------------------------- producer
     if (lane == 0) {
-      // raw pixels run up to kNu8 stages ahead: their slots free as soon as
+      // raw pixels run up to S::kNu8 stages ahead: their slots free as soon as
       // the converters have read them
       for (int st = 0; st < nst; ++st) {
-        const int pu = st % kNu8;
-        mbar_wait(&sm.u8_empty[pu], ((st / kNu8) & 1) ^ 1);
+        const int pu = st % S::kNu8;
+        mbar_wait(&sm.u8_empty[pu], ((st / S::kNu8) & 1) ^ 1);
         mbar_expect_tx(&sm.u8_full[pu], S::kU8);
-        tma_load_5d(sm.u8[pu], &tm_u8, &sm.u8_full[pu], 0, iw0, 2 * (st % 8), ih0,
+        tma_load_5d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], 0, iw0, 2 * (st % 8), ih0,
                     sm.slot[st / 8]);
       }
     } else if (lane == 1) {
       // weights follow the MMA-operand ring (independent thread, own waits)
-      mbar_expect_tx(&sm.wq_full, 192 * 64 * 2);
-      bulk_load(sm.wq, tcw.qkv0, 192 * 64 * 2, &sm.wq_full);
       for (int st = 0; st < nst; ++st) {
-        const int ps = st % kNst;
-        mbar_wait(&sm.empty[ps], ((st / kNst) & 1) ^ 1);
+        const int ps = st % S::kNst;
+        mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);
         mbar_expect_tx(&sm.w_full[ps], S::kW);
         bulk_load(sm.w[ps], tcw.emb + size_t(st) * tcw.emb_stage_elems, S::kW, &sm.w_full[ps]);
       }
+      // qkv weights into the A ring once the last embed MMA has read it
+      mbar_wait(&sm.acc_full, 0);
+      mbar_expect_tx(&sm.wq_full, 192 * 64 * 2);
+      bulk_load(sm.a(0), tcw.qkv0, 192 * 64 * 2, &sm.wq_full);
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA
     if (lane == 0) {
       const uint32_t idesc = idesc_f16(128, 64);
       for (int st = 0; st < nst; ++st) {
-        const int ps = st % kNst;
-        mbar_wait(&sm.aready[ps], (st / kNst) & 1);
-        mbar_wait(&sm.w_full[ps], (st / kNst) & 1);
+        const int ps = st % S::kNst;
+        mbar_wait(&sm.aready[ps], (st / S::kNst) & 1);
+        mbar_wait(&sm.w_full[ps], (st / S::kNst) & 1);
         tc_fence_after();
-        const uint32_t ab = smem_u32(sm.a[ps]), wb = smem_u32(sm.w[ps]);
+        const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w[ps]);
 #pragma unroll
         for (int kk = 0; kk < 2 * C; ++kk)
           mma_ss(tmem, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
@@ -158,8 +167,8 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       const uint32_t idesc2 = idesc_f16(128, 192);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        mma_ss(tmem + 64, sdesc(smem_u32(sm.a2) + kk * 4096, 128, kSwizzleNone, 2048),
-               sdesc(smem_u32(sm.wq) + kk * 6144, 128, kSwizzleNone, 3072), idesc2, kk != 0);
+        mma_ss(tmem + 64, sdesc(smem_u32(sm.u8(0)) + kk * 4096, 128, kSwizzleNone, 2048),
+               sdesc(smem_u32(sm.a(0)) + kk * 6144, 128, kSwizzleNone, 3072), idesc2, kk != 0);
       mma_commit(&sm.qkv_full);
     }
   } else {
@@ -172,15 +181,15 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     const bool masked = valid && a.rank[b * a.ns + s] >= 0;
     const bool last_slice = it == a.D.nt - 1;
     for (int st = 0; st < nst; ++st) {
-      const int ps = st % kNst, pu = st % kNu8;
-      mbar_wait(&sm.u8_full[pu], (st / kNu8) & 1);
-      if (st >= kNst) mbar_wait(&sm.empty[ps], ((st / kNst) & 1) ^ 1);   // A slot drained
+      const int ps = st % S::kNst, pu = st % S::kNu8;
+      mbar_wait(&sm.u8_full[pu], (st / S::kNu8) & 1);
+      if (st >= S::kNst) mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);   // A slot drained
       const bool zero = last_slice && (st / 8) == T - 1 && masked;   // corrupted frame
-      uint8_t* arow = sm.a[ps] + m * 16;
+      uint8_t* arow = sm.a(ps) + m * 16;
 #pragma unroll
       for (int pyl = 0; pyl < 2; ++pyl) {
         const uint4* src =
-            reinterpret_cast<const uint4*>(sm.u8[pu] + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
+            reinterpret_cast<const uint4*>(sm.u8(pu) + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           uint4 v = zero ? make_uint4(0, 0, 0, 0) : src[q];
@@ -235,7 +244,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
 #pragma unroll
     for (int o = 0; o < 64; ++o) var = fmaf(x[o] - mean, x[o] - mean, var);
     const float rstd = rsqrtf(var * (1.f / 64.f) + 1e-5f);
-    uint8_t* a2row = sm.a2 + m * 16;
+    uint8_t* a2row = sm.u8(0) + m * 16;   // every pixel stage has been consumed
 #pragma unroll
     for (int ki = 0; ki < 8; ++ki) {
       float y[8];
