@@ -264,17 +264,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 nm2 = make_float2(-mn, -mn);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32], pk[16];
-          tmem_ld32(t_s + 32 * ch, r);
+        for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
+          uint32_t r[64], pk[32];
+          tmem_ld32(t_s + 64 * h2, r);
+          tmem_ld32(t_s + 64 * h2 + 32, r + 32);
           tmem_wait_ld();
           if (valid < kTileK) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (32 * ch + c >= valid) r[c] = __float_as_uint(-INFINITY);
+            for (int c = 0; c < 64; ++c)
+              if (64 * h2 + c >= valid) r[c] = __float_as_uint(-INFINITY);
           }
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
+          for (int c = 0; c < 64; c += 2) {
             const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
                                    sc2, nm2);
             const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
@@ -282,7 +283,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
             pk[c >> 1] = pack_bf16(p.x, p.y);
           }
-          tmem_st16(t_s + 16 * ch, pk);
+          tmem_st16(t_s + 32 * h2, pk);
+          tmem_st16(t_s + 32 * h2 + 16, pk + 16);
         }
         l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
         m = mn;
