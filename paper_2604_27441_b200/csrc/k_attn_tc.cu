@@ -56,6 +56,7 @@ constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
 constexpr uint32_t kIdescS = idesc_bf16(128, 128);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buffer
+constexpr float kSlack = 8.f;                          // speculative-max headroom (log2)
 static_assert(kQT * 2 * kTileK <= 512, "TMEM budget");
 
 struct __align__(1024) Smem {
@@ -222,46 +223,32 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_wait(&sm.s_full[t][g & 1], (g >> 1) & 1);
         tc_fence_after();
         const int valid = a.ns - (j0 + j) * kTileK;   // keys of this tile that exist
-        // pass 1: row max of the raw scores (two 32-column loads in flight)
-        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // Running max: exact for the first key tile (pass 1), speculative
+        // afterwards -- P is computed against the running max while the
+        // tile's own max is tracked on the side; only a row whose max grew by
+        // more than kSlack (P > 2^kSlack) rescales its stored P by an exact
+        // power of two.  Softmax is shift-invariant, so this is the same sum.
+        float mn = m;
+        if (j == 0) {
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t r[64];
-          tmem_ld32(t_s + 64 * h, r);
-          tmem_ld32(t_s + 64 * h + 32, r + 32);
-          tmem_wait_ld();
-          if (valid >= kTileK) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
-          } else {
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[64];
+            tmem_ld32(t_s + 64 * h, r);
+            tmem_ld32(t_s + 64 * h + 32, r + 32);
+            tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 64; ++c)
               mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
           }
+          mn = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
         }
-        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-        const float mn = fmaxf(m, mx * a.scale_log2);
-        const float alpha = ex2(m - mn);
-        // fold O'(j-1) (ready: issued when this thread finished P(j-1)), then
-        // hand its buffer back for S(j+1)
-        if (j > 0) {
-          mbar_wait(&sm.pv_full[t], (g - 1) & 1);
-          tc_fence_after();
-          uint32_t ov[32];
-          tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
-          tmem_wait_ld();
-          const float2 ap = make_float2(a_prev, a_prev);
-#pragma unroll
-          for (int e = 0; e < kHd / 2; ++e)
-            o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
-                                                 __uint_as_float(ov[2 * e + 1])));
-          tc_fence_before();
-          mbar_arrive(&sm.o_read[t]);
-        }
-        // pass 2: p = 2^(s*scale - max) as packed bf16 pairs, written over the
-        // already-consumed S columns (chunk ch reads S[32ch, 32ch+32) and
-        // writes P pairs to columns [16ch, 16ch+16))
+        // exp pass: p = 2^(s*scale - mn) as packed bf16 pairs, written over the
+        // already-consumed S columns (chunk h2 reads S[64h2, 64h2+64) and
+        // writes P pairs to columns [32h2, 32h2+32)); O'(j-1) is folded
+        // between the two halves and its buffer handed back for S(j+1)
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float mt4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         const float2 nm2 = make_float2(-mn, -mn);
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
@@ -274,6 +261,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             for (int c = 0; c < 64; ++c)
               if (64 * h2 + c >= valid) r[c] = __float_as_uint(-INFINITY);
           }
+          if (j > 0) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) mt4[c & 3] = fmaxf(mt4[c & 3], __uint_as_float(r[c]));
+          }
 #pragma unroll
           for (int c = 0; c < 64; c += 2) {
             const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
@@ -285,8 +276,50 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           }
           tmem_st16(t_s + 32 * h2, pk);
           tmem_st16(t_s + 32 * h2 + 16, pk + 16);
+          if (h2 == 0 && j > 0) {
+            mbar_wait(&sm.pv_full[t], (g - 1) & 1);
+            tc_fence_after();
+            uint32_t ov[32];
+            tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
+            tmem_wait_ld();
+            const float2 ap = make_float2(a_prev, a_prev);
+#pragma unroll
+            for (int e = 0; e < kHd / 2; ++e)
+              o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
+                                                   __uint_as_float(ov[2 * e + 1])));
+            tc_fence_before();
+            mbar_arrive(&sm.o_read[t]);
+          }
         }
-        l = l * alpha + ((sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
+        float2 sums = fadd2(sum2[0], sum2[1]);
+        float tsum = sums.x + sums.y;
+        if (j > 0) {
+          const float mt = fmaxf(fmaxf(mt4[0], mt4[1]), fmaxf(mt4[2], mt4[3])) * a.scale_log2;
+          const bool grow = mt > mn + kSlack;
+          if (__any_sync(0xffffffffu, grow)) {
+            // rare: rescale this row's P (and its sum) by 2^-k, k integer
+            const float k = grow ? ceilf(mt - mn) : 0.f;
+            const float f = ex2(-k);
+            tmem_wait_st();
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              uint32_t pk[32];
+              tmem_ld32(t_s + 32 * h2, pk);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const float2 pv = unpack_bf16(pk[c]);
+                pk[c] = pack_bf16(pv.x * f, pv.y * f);
+              }
+              tmem_st16(t_s + 32 * h2, pk);
+              tmem_st16(t_s + 32 * h2 + 16, pk + 16);
+            }
+            tsum *= f;
+            mn += k;
+          }
+        }
+        const float alpha = ex2(m - mn);
+        l = l * alpha + tsum;
         m = mn;
         a_prev = alpha;
         tmem_wait_st();
