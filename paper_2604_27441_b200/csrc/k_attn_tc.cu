@@ -170,12 +170,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (j < nkv) {
             // S_t(j) into buf[t][j%2] once O'(j-2) there has been folded
             const int g = gkv + j, s = g % kStages;
-            mbar_wait(&sm.kv_full[s], (g / kStages) & 1);
+            mbar_wait_fast(&sm.kv_full[s], (g / kStages) & 1);
             tc_fence_after();
             const uint32_t kb = smem_u32(sm.k[s]);
             for (int t = 0; t < ntq; ++t) {
               if (j >= 2) {
-                mbar_wait(&sm.o_read[t], (go[t] + j - 2) & 1);
+                mbar_wait_fast(&sm.o_read[t], (go[t] + j - 2) & 1);
                 tc_fence_after();
               }
               for (int kk = 0; kk < 2; ++kk)
@@ -189,7 +189,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             const int jp = j - 1, sp = (gkv + jp) % kStages;
             const uint32_t vb = smem_u32(sm.v[sp]);
             for (int t = 0; t < ntq; ++t) {
-              mbar_wait(&sm.p_full[t], (gs[t] + jp) & 1);
+              mbar_wait_fast(&sm.p_full[t], (gs[t] + jp) & 1);
               tc_fence_after();
               const uint32_t bc = tmem + buf_col(t, gs[t] + jp);
               for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
