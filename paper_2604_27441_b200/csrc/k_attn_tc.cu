@@ -48,7 +48,11 @@ constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
 constexpr int kStages = 6;
 constexpr int kQT = 2;                                 // query tiles per CTA
-constexpr int kThreads = (4 * kQT + 2) * 32;           // softmax WGs + TMA + MMA
+constexpr int kThreads = (4 * kQT + 4) * 32;           // softmax WGs + (TMA, MMA, 2 idle)
+// Register split (setmaxnreg): the launch gives every thread 168 registers
+// (3 warps per SMSP); the TMA/MMA warpgroup drops to kRegsCtl and the two
+// softmax warpgroups rise to kRegsSoftmax (kRegsCtl + 2 kRegsSoftmax <= 512).
+constexpr int kRegsCtl = 40, kRegsSoftmax = 232;
 constexpr int kPolyOf4 = 1;                            // FMA-pipe exp2 pairs per 4
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
 constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
@@ -137,11 +141,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   //   gs[t]  S tiles of query slot t so far (buffer, s_full/p_full/pv_full phase)
   //   go[t]  O' folds of slot t so far (o_read phase)
   //   gq     groups so far (q_full, done phase)
+  // Each role runs its own copy of the group loop so that the register
+  // reallocation (setmaxnreg) covers disjoint code.
   int gkv = 0, gq = 0, gs[kQT] = {}, go[kQT] = {};
+  if (warp >= 4 * kQT) {
+    setmaxnreg_dec<kRegsCtl>();
   for (int group = group0; group * kQT * kTileQ < nq; group += kMulti ? a.groups : nq) {
     const int q0 = group * kQT * kTileQ;
     const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
-
     if (warp == kProducer) {
       // ---------------------------------------------------------- TMA producer
       if (lane == 0) {
@@ -204,7 +211,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mma_commit(&sm.done);             // the group's MMAs (Q reads) are complete
         mbar_wait(&sm.done, gq & 1);
       }
-    } else {
+    }
+    // next group: Q smem and TMEM are reused once everybody is done
+    if (!kMulti) break;
+    gkv += nkv;
+    ++gq;
+    for (int t = 0; t < ntq; ++t) {
+      gs[t] += nkv;
+      go[t] += nkv - 1;
+    }
+    tc_fence_before();
+    __syncwarp();
+    __syncthreads();
+    tc_fence_after();
+  }
+  } else {
+    setmaxnreg_inc<kRegsSoftmax>();
+  for (int group = group0; group * kQT * kTileQ < nq; group += kMulti ? a.groups : nq) {
+    const int q0 = group * kQT * kTileQ;
+    const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
+    {
       // ---------------------------------------------------------- softmax warps
       const int t = warp >> 2;                 // query tile
       const int quarter = warp & 3;            // TMEM lane quarter
@@ -373,6 +399,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     __syncwarp();
     __syncthreads();
     tc_fence_after();
+  }
   }
   tc_fence_before();
   __syncthreads();
