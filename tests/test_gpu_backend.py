@@ -152,3 +152,62 @@ def test_receiver_pipeline_matches_reference_receiver_chain():
         got, st = pipe.result(hnd)
         assert not st.any()
         assert np.array_equal(got, np.stack(expected))
+
+
+def test_concurrent_pinned_server_matches_engine():
+    """GPU front end (8f rank 2): several connections served concurrently
+    through pinned buffers return exactly what the per-request engine does,
+    including refs > k and the echo rules."""
+    import socket
+    import struct
+    import threading
+    from paper_2604_27441_b200.recovery import RecoveryEngine
+    from paper_2604_27441_b200.server import MSG_REQUEST, RecoveryServer
+    ck_r, _ = _ck(3, 505)
+    ck_d, _ = _ck(1, 506)
+    srv = RecoveryServer(("127.0.0.1", 0), checkpoint_rgb=ck_r, checkpoint_depth=ck_d,
+                         max_connections=4)
+    srv.start()
+    engines = {0: RecoveryEngine(ck_r.build_model(), "fast"),
+               1: RecoveryEngine(ck_d.build_model(), "fast")}
+    errors = []
+
+    def client(cid):
+        try:
+            rng = np.random.default_rng(cid)
+            sock = socket.create_connection(srv.addr, timeout=30.0)
+            (n,) = struct.unpack("<I", sock.recv(4))
+            sock.recv(n)
+            for it in range(4):
+                mod = (cid + it) % 2
+                c = 3 if mod == 0 else 1
+                h, w, k = 48, 64, [0, 2, 5, 7][it]
+                plane = textured_u8(rng, 1, h, w, c)[0]
+                refs = list(textured_u8(rng, k, h, w, c)) if k else []
+                grid = rng.random((h // 16, w // 16)) < 0.4
+                body = struct.pack("<BBIHHB", MSG_REQUEST, mod, it, w, h, k)
+                body += np.packbits(grid.reshape(-1)).tobytes() + plane.tobytes()
+                body += b"".join(r.tobytes() for r in refs)
+                sock.sendall(struct.pack("<I", len(body)) + body)
+                buf = b""
+                while len(buf) < 4:
+                    buf += sock.recv(4 - len(buf))
+                (n,) = struct.unpack("<I", buf)
+                resp = b""
+                while len(resp) < n:
+                    resp += sock.recv(n - len(resp))
+                got = np.frombuffer(resp[5:], np.uint8).reshape(h, w, c)
+                want = engines[mod].recover(plane, grid, refs) if refs and grid.any() else plane
+                if not np.array_equal(got, want.reshape(h, w, c)):
+                    errors.append((cid, it))
+            sock.close()
+        except Exception as exc:          # noqa: BLE001
+            errors.append((cid, repr(exc)))
+
+    threads = [threading.Thread(target=client, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(120)
+    srv.close()
+    assert not errors, errors
