@@ -594,8 +594,9 @@ def main():
                               "peak_exp_per_s": MUFU_PEAK,
                               "frac": (exps / (att_ms / 1000.0) / MUFU_PEAK) if att_ms else 0.0,
                               "note": "binding unit for head_dim 32 (128 MMA-FLOP per exp); "
-                                      "peak = 148 SM x 16 ex2/clk x 1.965 GHz (derived); "
-                                      "1/4 of the exps run as FMA-pipe polynomials"},
+                                      "peak = 148 SM x 16 ex2/clk x 1.965 GHz (15.9 ex2/clk/SM "
+                                      "measured by tools/ubench_xu.cu); 1/4 of the exps run as "
+                                      "FMA-pipe polynomials"},
                      "share_of_step": att_ms / max(1e-9, sum(prof.ms.values())),
                      "algorithmic_flops_per_launch": flops / max(1, att_launches)},
     }
