@@ -184,7 +184,9 @@ class NativeModel:
         need = self.lib.nvrec_workspace_bytes(self.handle, b, h, w, prec)
         if need < 0:
             check(int(need))
-        key = stream_ptr()
+        # per (stream, thread): two threads enqueueing on one stream would
+        # otherwise interleave their launches over a shared workspace
+        key = (stream_ptr(), threading.get_ident())
         ws = self._ws.get(key)
         if ws is None or ws.numel() < need:
             ws = torch.empty(int(need), dtype=torch.uint8, device=self.device)

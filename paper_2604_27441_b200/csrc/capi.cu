@@ -121,7 +121,7 @@ void transpose_into(std::vector<float>& dst, const float* w, int out, int in) {
 }
 
 struct WorkspaceLayout {
-  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, total;
+  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, redo, total;
 };
 
 WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
@@ -145,11 +145,14 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
     L.vth = take(seqrows * 2);
     L.q = L.k = L.v = SIZE_MAX;
     L.part = take(size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads * ns * 36 * 4);
+    // work items: query groups x splits x sequences (+ the count)
+    L.redo = take((1 + size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads *
+                   ((ns + 2 * nvrec::kAttnQTile - 1) / (2 * nvrec::kAttnQTile))) * 4);
   } else {
     L.q = take(seqrows * 4);
     L.k = take(seqrows * 4);
     L.v = take(seqrows * 4);
-    L.qh = L.kh = L.vth = L.part = SIZE_MAX;
+    L.qh = L.kh = L.vth = L.part = L.redo = SIZE_MAX;
   }
   L.list = take(size_t(b) * ns * 4);
   L.rank = take(size_t(b) * ns * 4);
@@ -192,6 +195,9 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
   dst.nt = D.nt; dst.ns = A.ns; dst.ns_pad = A.ns_pad; dst.d = D.d;
   dst.heads = D.heads; dst.hd = D.hd;
   dst.q = A.q; dst.k = A.k; dst.v = A.v; dst.qh = A.qh; dst.kh = A.kh; dst.vth = A.vth;
+  // arm the attention fix-up list once per forward (every fix-up launch
+  // leaves it empty again)
+  if (fast && A.redo_list) CK(cudaMemsetAsync(A.redo_list, 0, sizeof(int), s), "memset");
   for (int li = 0; li < D.layers; ++li) {
     const bool last = li == D.layers - 1;
     const bool prune_here = last && pruned;
@@ -462,6 +468,7 @@ static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout
   A.rank = at<int>(ws, L.rank);
   A.count = at<int>(ws, L.count);
   A.part = at<float>(ws, L.part);
+  A.redo_list = at<int>(ws, L.redo);
   A.b = b;
   A.nh = h / m->D.p;
   A.nw = w / m->D.p;

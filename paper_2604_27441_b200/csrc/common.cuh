@@ -78,6 +78,7 @@ struct Act {
   int* rank;         // [b][ns] position -> row in list, -1 if absent
   int* count;        // [b] entries in list
   float* part;       // bf16 path: key-split attention partials [split][seq][ns][36]
+  int* redo_list;    // bf16 path: [0] count + attention work items for the exact fix-up
   int b, ns, nh, nw, ns_pad;
 };
 constexpr int kAttnMaxSplits = 3;

@@ -30,6 +30,7 @@
 // 8d): MUFU ex2 for most pairs, the FMA-pipe polynomial for one pair in
 // kPolyOf4 of each four.
 #include <cstdlib>
+#include <type_traits>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -60,7 +61,7 @@ constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
 constexpr uint32_t kIdescS = idesc_bf16(128, 128);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buffer
-constexpr float kSlack = 8.f;                          // speculative-max headroom (log2)
+constexpr float kSlackSum = 256.f;                     // speculative-max headroom: row sum of P
 static_assert(kQT * 2 * kTileK <= 512, "TMEM budget");
 
 struct __align__(1024) Smem {
@@ -70,6 +71,7 @@ struct __align__(1024) Smem {
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
   uint64_t s_full[kQT][2], p_full[kQT], pv_full[kQT], o_read[kQT], done;
+  int redo[3];                      // per group iteration (mod 3): speculative max overflowed
   uint32_t tmem_base;
 };
 
@@ -80,15 +82,22 @@ struct TcArgs {
   int nt, heads, ns, d, seqs;
   int splits;         // key-range splits (flash-decoding style) >= 1
   int groups;         // query groups launched per (seq, split); CTAs loop
+  int mode;           // 0 speculative max (default), 1 exact maxima, 2 force redo (tests)
+  int* redo_list;     // [0] = count, then work items whose speculative max overflowed
   float scale_log2;
 };
 constexpr int kPart = 36;                              // 32 output dims, m, l, 2 pad (16 B rows)
 
 __device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 * t + (j & 1)) * kTileK); }
 
-// kMulti: the CTA may loop over several query groups (pruned launches); the
-// dense instantiation runs exactly one group and keeps every counter at 0.
-template <bool kMulti>
+// Work item = (query group, key split, sequence), it = (group*splits + split)*seqs + seq.
+// kMulti: the CTA may loop over several items (pruned launches step through a
+// stream's query groups; the fix-up launch walks redo_list); the dense
+// instantiation runs exactly one item and keeps every counter at 0.
+// kExact: exact per-tile maxima (the fix-up); otherwise the speculative
+// running max, and a CTA whose exponent overflowed records its item for the
+// fix-up launch that follows on the same stream.
+template <bool kMulti, bool kExact, bool kList>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_k,
@@ -96,20 +105,36 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // query-group-major order: every sequence's (short) last group runs last
-  const int seq = blockIdx.x % a.seqs;
-  const int split = (blockIdx.x / a.seqs) % a.splits;
-  const int group0 = blockIdx.x / (a.seqs * a.splits);
-  const int b = seq / (a.nt * a.heads);
-  const int nq = a.count ? a.count[b] : a.ns;
-  if (group0 * kQT * kTileQ >= nq) return;                // uniform across the CTA
   const int nkv_all = (a.ns + kTileK - 1) / kTileK;
-  const int j0 = split * nkv_all / a.splits;              // this CTA's key tiles
-  const int nkv = (split + 1) * nkv_all / a.splits - j0;
+  const int n_list = kList ? a.redo_list[0] : 0;
+  if (kList && n_list == 0) return;                       // nothing overflowed (uniform)
+  // the k-th work item of this CTA, or -1 when done
+  auto item_at = [&](int k) -> int {
+    if (kList) return k < n_list ? a.redo_list[1 + k] : -1;
+    if (!kMulti && k > 0) return -1;
+    return int(blockIdx.x) + k * int(gridDim.x);
+  };
+  struct Item { int seq, split, group, b, nq, j0, nkv; };
+  auto decode = [&](int it) {
+    Item w;
+    w.seq = it % a.seqs;
+    w.split = (it / a.seqs) % a.splits;
+    w.group = it / (a.seqs * a.splits);
+    w.b = w.seq / (a.nt * a.heads);
+    w.nq = a.count ? a.count[w.b] : a.ns;
+    w.j0 = w.split * nkv_all / a.splits;
+    w.nkv = (w.split + 1) * nkv_all / a.splits - w.j0;
+    return w;
+  };
+  // an item past its stream's queries: skip it (list) or stop (grid order)
+  auto live = [&](const Item& w) { return w.group * kQT * kTileQ < w.nq; };
+  if (!kList && !live(decode(blockIdx.x))) return;        // uniform across the CTA
 
   const int kProducer = 4 * kQT, kMma = 4 * kQT + 1;
   if (warp == kProducer && lane == 0) {
     mbar_init(&sm.done, 1);
+    sm.redo[0] = (a.mode == 2 && !kExact) ? 1 : 0;   // mode 2: the first item is redone
+    sm.redo[1] = sm.redo[2] = 0;
     mbar_init(&sm.q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.kv_full[s], 1);
@@ -146,12 +171,21 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   int gkv = 0, gq = 0, gs[kQT] = {}, go[kQT] = {};
   if (warp >= 4 * kQT) {
     setmaxnreg_dec<kRegsCtl>();
-  for (int group = group0; group * kQT * kTileQ < nq; group += kMulti ? a.groups : nq) {
-    const int q0 = group * kQT * kTileQ;
+  for (int kit = 0;; ++kit) {
+    const int it = item_at(kit);
+    if (it < 0) break;
+    const Item w = decode(it);
+    if (!live(w)) {
+      if (kList) continue;
+      break;
+    }
+    const int seq = w.seq, split = w.split, b = w.b, nq = w.nq, j0 = w.j0, nkv = w.nkv;
+    const int q0 = w.group * kQT * kTileQ;
     const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
     if (warp == kProducer) {
       // ---------------------------------------------------------- TMA producer
       if (lane == 0) {
+        sm.redo[(gq + 1) % 3] = 0;                 // slot of iteration gq+1 (last read at gq-2)
         mbar_expect_tx(&sm.q_full, ntq * kQBytes);
         for (int t = 0; t < ntq; ++t)
           tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
@@ -212,8 +246,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_wait(&sm.done, gq & 1);
       }
     }
-    // next group: Q smem and TMEM are reused once everybody is done
-    if (!kMulti) break;
+    // next group (or the same one again, exact, if a speculative max
+    // overflowed): Q smem and TMEM are reused once everybody is done
+    const int gq_done = gq;
     gkv += nkv;
     ++gq;
     for (int t = 0; t < ntq; ++t) {
@@ -224,11 +259,23 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     __syncwarp();
     __syncthreads();
     tc_fence_after();
+    if (!kExact && warp == kProducer && lane == 0 && sm.redo[gq_done % 3] != 0) {
+      const int idx = atomicAdd(a.redo_list, 1);     // overflowed: exact fix-up later
+      a.redo_list[1 + idx] = it;
+    }
   }
   } else {
     setmaxnreg_inc<kRegsSoftmax>();
-  for (int group = group0; group * kQT * kTileQ < nq; group += kMulti ? a.groups : nq) {
-    const int q0 = group * kQT * kTileQ;
+  for (int kit = 0;; ++kit) {
+    const int it = item_at(kit);
+    if (it < 0) break;
+    const Item w = decode(it);
+    if (!live(w)) {
+      if (kList) continue;
+      break;
+    }
+    const int seq = w.seq, split = w.split, b = w.b, nq = w.nq, j0 = w.j0, nkv = w.nkv;
+    const int q0 = w.group * kQT * kTileQ;
     const int ntq = min(kQT, (nq - q0 + kTileQ - 1) / kTileQ);   // live query tiles
     {
       // ---------------------------------------------------------- softmax warps
@@ -243,115 +290,129 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
       const int gst = gs[t];
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
-      for (int j = 0; j < jend; ++j) {
-        const int g = gst + j;
-        const uint32_t t_s = tmem + lane_off + buf_col(t, g);
-        mbar_wait(&sm.s_full[t][g & 1], (g >> 1) & 1);
-        tc_fence_after();
-        const int valid = a.ns - (j0 + j) * kTileK;   // keys of this tile that exist
-        // Running max: exact for the first key tile (pass 1), speculative
-        // afterwards -- P is computed against the running max while the
-        // tile's own max is tracked on the side; only a row whose max grew by
-        // more than kSlack (P > 2^kSlack) rescales its stored P by an exact
-        // power of two.  Softmax is shift-invariant, so this is the same sum.
-        float mn = m;
-        if (j == 0) {
-          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t r[64];
-            tmem_ld32(t_s + 64 * h, r);
-            tmem_ld32(t_s + 64 * h + 32, r + 32);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
-          }
-          mn = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
-        }
-        // exp pass: p = 2^(s*scale - mn) as packed bf16 pairs, written over the
-        // already-consumed S columns (chunk h2 reads S[64h2, 64h2+64) and
-        // writes P pairs to columns [32h2, 32h2+32)); O'(j-1) is folded
-        // between the two halves and its buffer handed back for S(j+1)
-        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        float mt4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        const float2 nm2 = make_float2(-mn, -mn);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
-          uint32_t r[64], pk[32];
-          tmem_ld32(t_s + 64 * h2, r);
-          tmem_ld32(t_s + 64 * h2 + 32, r + 32);
-          tmem_wait_ld();
-          if (valid < kTileK) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (64 * h2 + c >= valid) r[c] = __float_as_uint(-INFINITY);
-          }
-          if (j > 0) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) mt4[c & 3] = fmaxf(mt4[c & 3], __uint_as_float(r[c]));
-          }
-#pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
-                                   sc2, nm2);
-            const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
-                                                       : make_float2(ex2(v.x), ex2(v.y));
-            sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
-            pk[c >> 1] = pack_bf16(p.x, p.y);
-          }
-          tmem_st16(t_s + 32 * h2, pk);
-          tmem_st16(t_s + 32 * h2 + 16, pk + 16);
-          if (h2 == 0 && j > 0) {
-            mbar_wait(&sm.pv_full[t], (g - 1) & 1);
-            tc_fence_after();
-            uint32_t ov[32];
-            tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
-            tmem_wait_ld();
-            const float2 ap = make_float2(a_prev, a_prev);
-#pragma unroll
-            for (int e = 0; e < kHd / 2; ++e)
-              o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
-                                                   __uint_as_float(ov[2 * e + 1])));
-            tc_fence_before();
-            mbar_arrive(&sm.o_read[t]);
-          }
-        }
-        float2 sums = fadd2(sum2[0], sum2[1]);
-        float tsum = sums.x + sums.y;
-        if (j > 0) {
-          const float mt = fmaxf(fmaxf(mt4[0], mt4[1]), fmaxf(mt4[2], mt4[3])) * a.scale_log2;
-          const bool grow = mt > mn + kSlack;
-          if (__any_sync(0xffffffffu, grow)) {
-            // rare: rescale this row's P (and its sum) by 2^-k, k integer
-            const float k = grow ? ceilf(mt - mn) : 0.f;
-            const float f = ex2(-k);
-            tmem_wait_st();
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              uint32_t pk[32];
-              tmem_ld32(t_s + 32 * h2, pk);
+      // the key-tile loop, specialised for speculative / exact maxima
+      // (Z: counters known to be zero -- the single speculative pass of a
+      // dense CTA -- so buffer/phase arithmetic folds at compile time)
+      auto tiles = [&](auto ex_tag, auto zero_tag) {
+        constexpr bool EX = decltype(ex_tag)::value;
+        constexpr bool Z = decltype(zero_tag)::value;
+        const int gst0 = Z ? 0 : gst;
+        for (int j = 0; j < jend; ++j) {
+          const int g = gst0 + j;
+          const uint32_t t_s = tmem + lane_off + buf_col(t, g);
+          mbar_wait(&sm.s_full[t][g & 1], (g >> 1) & 1);
+          tc_fence_after();
+          const int valid = a.ns - (j0 + j) * kTileK;   // keys of this tile that exist
+          // Running max: exact for the first key tile (pass 1), speculative
+          // afterwards -- P is computed against the running max while the
+          // tile's own max is tracked on the side; only a row whose max grew by
+          // more than kSlack (P > 2^kSlack) rescales its stored P by an exact
+          // power of two.  Softmax is shift-invariant, so this is the same sum.
+          float mn = m;
+          if (j == 0 || EX) {
+            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[64];
+              tmem_ld32(t_s + 64 * h, r);
+              tmem_ld32(t_s + 64 * h + 32, r + 32);
               tmem_wait_ld();
-#pragma unroll
+  #pragma unroll
+              for (int c = 0; c < 64; ++c)
+                mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+            }
+            mn = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2);
+          }
+          // exp pass: p = 2^(s*scale - mn) as packed bf16 pairs, written over the
+          // already-consumed S columns (chunk h2 reads S[64h2, 64h2+64) and
+          // writes P pairs to columns [32h2, 32h2+32)); O'(j-1) is folded
+          // between the two halves and its buffer handed back for S(j+1)
+          float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          const float2 nm2 = make_float2(-mn, -mn);
+  #pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
+            uint32_t r[64], pk[32];
+            tmem_ld32(t_s + 64 * h2, r);
+            tmem_ld32(t_s + 64 * h2 + 32, r + 32);
+            tmem_wait_ld();
+            if (valid < kTileK) {
+  #pragma unroll
+              for (int c = 0; c < 64; ++c)
+                if (64 * h2 + c >= valid) r[c] = __float_as_uint(-INFINITY);
+            }
+  #pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+              const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                     sc2, nm2);
+              const float2 p = ((c >> 1) & 3) < kPolyOf4 ? exp2_poly2(v)
+                                                         : make_float2(ex2(v.x), ex2(v.y));
+              sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+              pk[c >> 1] = pack_bf16(p.x, p.y);
+            }
+            tmem_st16(t_s + 32 * h2, pk);
+            tmem_st16(t_s + 32 * h2 + 16, pk + 16);
+            if (h2 == 0 && j > 0) {
+              mbar_wait(&sm.pv_full[t], (g - 1) & 1);
+              tc_fence_after();
+              uint32_t ov[32];
+              tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
+              tmem_wait_ld();
+              const float2 ap = make_float2(a_prev, a_prev);
+  #pragma unroll
+              for (int e = 0; e < kHd / 2; ++e)
+                o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
+                                                     __uint_as_float(ov[2 * e + 1])));
+              tc_fence_before();
+              mbar_arrive(&sm.o_read[t]);
+            }
+          }
+          float2 sums = fadd2(sum2[0], sum2[1]);
+          float tsum = sums.x + sums.y;
+          if (!EX && j > 0 && __any_sync(0xffffffffu, tsum > kSlackSum)) {
+            // rare: the row sum exceeds 2^kSlack, so some p may too -- rescale
+            // this row's P (and its sum) by 2^-k, k = ceil(log2 max p), exact
+            tmem_wait_st();
+            uint32_t pk[2][32];
+            float pmax = 0.f;
+  #pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              tmem_ld32(t_s + 32 * h2, pk[h2]);
+              tmem_wait_ld();
+  #pragma unroll
               for (int c = 0; c < 32; ++c) {
-                const float2 pv = unpack_bf16(pk[c]);
-                pk[c] = pack_bf16(pv.x * f, pv.y * f);
+                const float2 pv = unpack_bf16(pk[h2][c]);
+                pmax = fmaxf(pmax, fmaxf(pv.x, pv.y));
               }
-              tmem_st16(t_s + 32 * h2, pk);
-              tmem_st16(t_s + 32 * h2 + 16, pk + 16);
+            }
+            // p >= 2^100 (or inf from MUFU): the exponent overflowed, P is not
+            // exact any more -> the whole query group is redone with exact maxima
+            if (tsum > kSlackSum && !(pmax < 0x1p100f)) sm.redo[gq % 3] = 1;
+            const float k = tsum > kSlackSum && pmax < 0x1p100f ? fmaxf(0.f, ceilf(__log2f(pmax)))
+                                                                : 0.f;
+            const float f = ex2(-k);
+  #pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+  #pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const float2 pv = unpack_bf16(pk[h2][c]);
+                pk[h2][c] = pack_bf16(pv.x * f, pv.y * f);
+              }
+              tmem_st16(t_s + 32 * h2, pk[h2]);
+              tmem_st16(t_s + 32 * h2 + 16, pk[h2] + 16);
             }
             tsum *= f;
             mn += k;
           }
+          const float alpha = ex2(m - mn);
+          l = l * alpha + tsum;
+          m = mn;
+          a_prev = alpha;
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.p_full[t]);
         }
-        const float alpha = ex2(m - mn);
-        l = l * alpha + tsum;
-        m = mn;
-        a_prev = alpha;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&sm.p_full[t]);
-      }
+      };
+      tiles(std::integral_constant<bool, kExact>{}, std::integral_constant<bool, !kMulti>{});
       const int q = q0 + t * kTileQ + row;
       if (t < ntq) {
         const int g = gst + nkv - 1;
@@ -387,8 +448,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         }
       }
     }
-    // next group: Q smem and TMEM are reused once everybody is done
-    if (!kMulti) break;
+    // next group (or the same one again, exact, if a speculative max
+    // overflowed): Q smem and TMEM are reused once everybody is done
+    const int gq_done = gq;
     gkv += nkv;
     ++gq;
     for (int t = 0; t < ntq; ++t) {
@@ -399,11 +461,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     __syncwarp();
     __syncthreads();
     tc_fence_after();
+    (void)gq_done;
   }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
+  if (kList && threadIdx.x == 0) a.redo_list[0] = 0;      // single fix-up CTA: re-arm
 }
 
 // Merge the key-range partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
@@ -490,8 +554,14 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   const size_t smem = sizeof(Smem) + 1024;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(attn_tc_kernel<false, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(attn_tc_kernel<true, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -516,9 +586,24 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   }
   if (force >= 1 && force <= kAttnMaxSplits && force <= nkv && A.part) best = force;
   ta.splits = best;
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("NVREC_ATTN_MODE");        // tests: exact / redo
+    mode = e && e[0] == 'e' ? 1 : (e && e[0] == 'r' ? 2 : 0);
+  }
+  ta.mode = mode;
+  ta.redo_list = A.redo_list;
   dim3 grid(ta.groups * seqs * ta.splits);
-  if (count) attn_tc_kernel<true><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
-  else attn_tc_kernel<false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  if (mode == 1 || !A.redo_list) {
+    // exact maxima throughout (tests), or no fix-up list available
+    attn_tc_kernel<true, true, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+  } else {
+    if (count) attn_tc_kernel<true, false, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+    else attn_tc_kernel<false, false, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+    // exact fix-up of the (rare) items whose speculative exponent overflowed;
+    // one CTA, exits at once when the list is empty, re-arms the list count
+    attn_tc_kernel<true, true, true><<<1, kThreads, smem, s>>>(tq, tk, tv, ta);
+  }
   if (ta.splits > 1) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
     attn_combine_kernel<<<cg, 256, 0, s>>>(A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,

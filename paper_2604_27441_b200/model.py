@@ -13,6 +13,8 @@ outside the recovery path).
 
 from __future__ import annotations
 
+import threading
+
 import torch
 from torch import nn
 
@@ -64,6 +66,7 @@ class MaskedVideoModel(nn.Module):
         self.head = nn.Linear(d, t * p * p * channels)
         self._native = None
         self._packed_sig = None
+        self._native_lock = threading.Lock()
 
     # -- weights -> device ----------------------------------------------------
 
@@ -76,13 +79,18 @@ class MaskedVideoModel(nn.Module):
         """The packed on-device model, re-packed when any parameter changed."""
         dev = _native.require_cuda(device)
         sig = self._signature()
-        if self._native is None or self._native.device != dev:
-            self._native = _native.NativeModel(self.config, self.channels, dev)
-            self._packed_sig = None
-        if self._packed_sig != sig:
-            self._native.load(list(self.state_dict().values()))
-            self._packed_sig = sig
-        return self._native
+        nat = self._native
+        if nat is not None and nat.device == dev and self._packed_sig == sig:
+            return nat
+        # serving threads share one model: create / re-pack exactly once
+        with self._native_lock:
+            if self._native is None or self._native.device != dev:
+                self._native = _native.NativeModel(self.config, self.channels, dev)
+                self._packed_sig = None
+            if self._packed_sig != sig:
+                self._native.load(list(self.state_dict().values()))
+                self._packed_sig = sig
+            return self._native
 
     # -- forward -------------------------------------------------------------
 

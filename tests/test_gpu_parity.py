@@ -206,3 +206,28 @@ def test_fast_vs_reference_error_budget_720p():
         err = np.abs(got - want)
         print("c=%d precise max-abs %.2e (x65535 = %.3f)" % (c, err.max(), err.max() * 65535))
         assert err.max() * 65535 <= 1.0
+
+
+def _attn_mode_run(mode, path):
+    import subprocess
+    import sys
+    env = dict(os.environ, NVREC_ATTN_MODE=mode)
+    here = os.path.dirname(os.path.abspath(__file__))
+    subprocess.run([sys.executable, os.path.join(here, "attn_mode_probe.py"), path],
+                   check=True, env=env, timeout=300)
+    return np.load(path)
+
+
+def test_speculative_max_matches_exact_maxima(tmp_path):
+    """The speculative running max (no max pass after the first key tile) is
+    the same softmax as exact per-tile maxima: u8 outputs within 1 LSB; the
+    forced redo path (exact recompute of a query group) reproduces the exact
+    mode bit for bit; with sharply scaled scores (exponent overflow -> group
+    redo) the result stays finite and matches the exact mode."""
+    spec = _attn_mode_run("spec", str(tmp_path / "s.npz"))
+    exact = _attn_mode_run("exact", str(tmp_path / "e.npz"))
+    redo = _attn_mode_run("redo", str(tmp_path / "r.npz"))
+    assert np.abs(spec["out"].astype(int) - exact["out"].astype(int)).max() <= 1
+    assert np.array_equal(redo["out"], exact["out"])
+    assert np.isfinite(spec["sharp"]).all()
+    assert np.abs(spec["sharp"] - exact["sharp"]).max() <= 1e-3
