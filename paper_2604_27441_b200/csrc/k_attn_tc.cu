@@ -368,7 +368,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           }
           float2 sums = fadd2(sum2[0], sum2[1]);
           float tsum = sums.x + sums.y;
-          if (!EX && j > 0 && __any_sync(0xffffffffu, tsum > kSlackSum)) {
+          if (!EX && j > 0 && __any_sync(0xffffffffu, !(tsum <= kSlackSum))) {
             // rare: the row sum exceeds 2^kSlack, so some p may too -- rescale
             // this row's P (and its sum) by 2^-k, k = ceil(log2 max p), exact
             tmem_wait_st();
@@ -386,7 +386,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             }
             // p >= 2^100 (or inf from MUFU): the exponent overflowed, P is not
             // exact any more -> the whole query group is redone with exact maxima
-            if (tsum > kSlackSum && !(pmax < 0x1p100f)) sm.redo[gq % 3] = 1;
+            if (!(tsum <= kSlackSum) && !(pmax < 0x1p100f)) sm.redo[gq % 3] = 1;
             const float k = tsum > kSlackSum && pmax < 0x1p100f ? fmaxf(0.f, ceilf(__log2f(pmax)))
                                                                 : 0.f;
             const float f = ex2(-k);

@@ -251,8 +251,8 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // j to the exponent field.  Since (bits(1.5*2^23) << 23) == 0 mod 2^32, the
 // exponent add is a single IMAD: bits(p) + bits(t) * 2^23.
 __device__ __forceinline__ float2 exp2_poly2(float2 v) {
-  v.x = fmaxf(v.x, -127.f);
-  v.y = fmaxf(v.y, -127.f);
+  v.x = fminf(fmaxf(v.x, -127.f), 127.f);    // the exponent add must not wrap
+  v.y = fminf(fmaxf(v.y, -127.f), 127.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);
   const float2 nmagic = make_float2(-12582912.f, -12582912.f);
   const float2 t = fadd2(v, magic);
