@@ -205,8 +205,9 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
 
 /* Optional per-stage timing for benchmarks: between begin and end every
  * kernel launch is bracketed by CUDA events on its stream; end synchronises
- * and returns the summed milliseconds and launch counts per NVREC_STAGE_*.
- * Returns the number of timed launches.  Not thread-safe; off by default. */
+ * and returns the summed milliseconds and kernel-launch counts per
+ * NVREC_STAGE_*.  Returns the number of kernels launched.  Not thread-safe;
+ * off by default. */
 enum {
   NVREC_STAGE_LOSSMASK = 0, NVREC_STAGE_MASKLIST = 1, NVREC_STAGE_COPY = 2,
   NVREC_STAGE_EMBED = 3, NVREC_STAGE_LNQKV = 4, NVREC_STAGE_ATTN_SIMT = 5,

@@ -43,7 +43,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 // durations per stage.  Off by default (zero overhead on the hot path).
 namespace {
 constexpr int kProfMax = 8192;
-struct ProfRec { cudaEvent_t a, b; int kind; };
+struct ProfRec { cudaEvent_t a, b; int kind, kernels; };
 bool g_prof = false;
 std::vector<ProfRec> g_prof_pool;
 int g_prof_n = 0;
@@ -55,8 +55,11 @@ struct ProfScope {
     if (!g_prof || g_prof_n >= int(g_prof_pool.size())) return;
     r = &g_prof_pool[g_prof_n++];
     r->kind = kind;
+    r->kernels = 1;
     cudaEventRecord(r->a, s);
   }
+  // kernels launched inside this scope (default one)
+  void kernels(int n) { if (r) r->kernels = n; }
   ~ProfScope() { if (r) cudaEventRecord(r->b, s); }
 };
 }  // namespace
@@ -205,7 +208,9 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     cudaError_t e;
     if (fast) {
       ProfScope ps(NVREC_STAGE_ATTN_TC, s);
-      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s);
+      int nk = 1;
+      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk);
+      ps.kernels(nk);
     } else {
       nvrec::AttnArgs aa{};
       aa.q = A.q; aa.k = A.k; aa.v = A.v; aa.ao = A.ao;
@@ -607,6 +612,7 @@ int nvrec_decode(const nvrec_decode_job* jobs, int32_t n_jobs, int32_t max_block
   cudaError_t e;
   {
     ProfScope ps(NVREC_STAGE_DECODE, static_cast<cudaStream_t>(stream));
+    ps.kernels(3);
     e = nvrec::launch_decode(jobs, n_jobs, max_blocks, static_cast<cudaStream_t>(stream));
   }
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");
@@ -670,6 +676,7 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
   cudaError_t e;
   {
     ProfScope ps(NVREC_STAGE_BASELINE, s);
+    ps.kernels(depth ? 3 : 1);
     e = nvrec::launch_baseline(depth, b, h, w, c, planes, refs, mask_bits, out, base, list,
                                rank, count, bbox, s);
   }
@@ -700,10 +707,11 @@ int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t 
     CK(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
     if (r.kind >= 0 && r.kind < n_stages) {
       ms_per_stage[r.kind] += ms;
-      launches_per_stage[r.kind] += 1;
+      launches_per_stage[r.kind] += r.kernels;
     }
   }
-  int n = g_prof_n;
+  int n = 0;
+  for (int i = 0; i < g_prof_n; ++i) n += g_prof_pool[i].kernels;
   g_prof_n = 0;
   return n;
 }

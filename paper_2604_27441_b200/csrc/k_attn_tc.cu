@@ -528,7 +528,8 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 
 bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
-cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s) {
+cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
+                           int* n_kernels) {
   const int seqs = A.b * D.nt * D.heads;
   CUtensorMap tq, tk, tv;
   const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
@@ -604,6 +605,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
     // one CTA, exits at once when the list is empty, re-arms the list count
     attn_tc_kernel<true, true, true><<<1, kThreads, smem, s>>>(tq, tk, tv, ta);
   }
+  if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (ta.splits > 1 ? 1 : 0);
   if (ta.splits > 1) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
     attn_combine_kernel<<<cg, 256, 0, s>>>(A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,

@@ -98,7 +98,8 @@ cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index,
                               size_t frame_bytes, uint8_t* out, int b, cudaStream_t s);
 cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_t s);
-cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s);
+cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
+                           int* n_kernels = nullptr);
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
