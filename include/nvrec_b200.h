@@ -159,7 +159,7 @@ typedef struct nvrec_decode_job {
   const uint8_t* reference;
   uint8_t* plane;
   int64_t plane_capacity;     /* bytes available at plane                     */
-  int32_t* scratch;           /* int32[mask.grid_capacity + 4] device scratch */
+  int32_t* scratch;           /* int32[2 * mask.grid_capacity + 4] device scratch */
 } nvrec_decode_job;
 
 /* Batched decode: jobs is a DEVICE array; max_blocks >= every job's block

@@ -13,7 +13,7 @@ Drop-in for the two reference steps that produce the recovery path's input:
 
 Both are thin hosts around ``nvrec_decode`` / ``nvrec_rs_plan`` +
 ``nvrec_rs_reconstruct`` (k_decode.cu, k_rs.cu).  ``DecodeBatch`` is the
-serving form: fixed-capacity pinned staging, one H2D copy and three kernel
+serving form: fixed-capacity pinned staging, one H2D copy and four kernel
 launches for a batch of frames, outputs (planes, grids, wire bitsets) left on
 the device for ``nvrec_recover_u8``.
 """
@@ -126,7 +126,7 @@ class DecodeBatch:
         self.wire = torch.zeros((max_jobs, self.wire_stride), dtype=torch.uint8,
                                 device=self.device)
         self.status = torch.zeros((max_jobs, 4), dtype=torch.int32, device=self.device)
-        self.scratch = torch.zeros((max_jobs, max_blocks + 4), dtype=torch.int32,
+        self.scratch = torch.zeros((max_jobs, 2 * max_blocks + 4), dtype=torch.int32,
                                    device=self.device)
         self._jobs = (_native.DecodeJob * max_jobs)()
         self.n = 0

@@ -612,7 +612,7 @@ int nvrec_decode(const nvrec_decode_job* jobs, int32_t n_jobs, int32_t max_block
   cudaError_t e;
   {
     ProfScope ps(NVREC_STAGE_DECODE, static_cast<cudaStream_t>(stream));
-    ps.kernels(3);
+    ps.kernels(4);
     e = nvrec::launch_decode(jobs, n_jobs, max_blocks, static_cast<cudaStream_t>(stream));
   }
   if (e != cudaSuccess) return cuda_fail(e, "decode launch");

@@ -11,11 +11,13 @@
 // clean blocks, channel-planar within a block (codec.py:85-96,296-317);
 // every other block keeps the reference (P) or zero (I).
 //
-// Three launches per batch of frames:
+// Four launches per batch of frames:
 //   decode_parse_kernel   one CTA per frame: lm::lossmask_job (the mask path
 //                         of k_lossmask.cu) + per-block present rank table.
-//   decode_blocks_kernel  one warp per 16x16 block: copies the reference
-//                         block, or RLE-decodes the block's own payload range
+//   decode_copy_kernel    base plane: the reference (P) or zeros (I), 16 B
+//                         per thread, grid-stride (HBM-bound).
+//   decode_present_kernel one warp per present block: RLE-decodes the block's
+//                         own payload range
 //                         (warp scan of the run lengths, run starts marked in
 //                         shared memory, carry-forward scan) and writes the
 //                         reconstructed pixels.  Exact whenever every clean
@@ -28,7 +30,7 @@
 //                         the literal reference semantics (python slicing of
 //                         each range, concatenation, records straddling
 //                         ranges, the two error checks in reference order).
-// All three are stream-ordered and graph capturable; nothing syncs the host.
+// All four are stream-ordered and graph capturable; nothing syncs the host.
 #include "launch.cuh"
 #include "lossmask.cuh"
 
@@ -91,7 +93,7 @@ decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
   const nvrec_decode_job job = jobs[blockIdx.x];
   lm::Header H;
   int err = lm::lossmask_job(job.mask, job.scratch + 4, &H, sh_scan, &sh_flagged, stage,
-                             kParseStage);
+                             kParseStage, job.scratch + 4 + job.mask.grid_capacity);
   if (threadIdx.x == 0) {
     if (!err && H.kind == 1 && !job.reference) err = lm::kNeedReference;
     if (!err && int64_t(H.h) * H.w * H.channels > job.plane_capacity) err = lm::kPlaneCapacity;
@@ -100,15 +102,37 @@ decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
   }
 }
 
+// Base plane: the reference (P) or zeros (I), grid-stride, 16 B per thread
+// where aligned; clean present blocks are overwritten by the next kernel.
 __global__ void __launch_bounds__(kThreads)
-decode_blocks_kernel(const nvrec_decode_job* __restrict__ jobs) {
-  __shared__ uint32_t sh_mark[kWarps][kMaxBs];
+decode_copy_kernel(const nvrec_decode_job* __restrict__ jobs) {
   const nvrec_decode_job& jr = jobs[blockIdx.y];
   if (jr.mask.status[0] != 0) return;
   const Fixed f = read_fixed(jr.mask.header);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * kWarps + warp;
-  if (j >= f.n_blocks) return;
+  const uint8_t* ref = jr.reference;
+  uint8_t* out = jr.plane;
+  if (f.kind == 1 && ref == out) return;                 // in-place decode
+  const size_t bytes = size_t(f.h) * f.w * f.c;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  const size_t t0 = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(ref) | reinterpret_cast<uintptr_t>(out) | bytes) & 15) == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(ref);
+    uint4* dst = reinterpret_cast<uint4*>(out);
+    for (size_t i = t0; i < bytes / 16; i += stride)
+      dst[i] = f.kind == 1 ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+  } else {
+    for (size_t i = t0; i < bytes; i += stride) out[i] = f.kind == 1 ? ref[i] : 0;
+  }
+}
+
+// One present block (rank r) per warp: RLE-decode the block's own payload
+// range and write reference + delta (P) / value (I).
+__device__ __forceinline__ void decode_one(const nvrec_decode_job& jr, const Fixed& f, int r,
+                                           uint32_t* mk, uint8_t* rec, int lane) {
+  __syncwarp();                                        // previous block's buffers drained
+  const int32_t pid = jr.scratch[4 + jr.mask.grid_capacity + r];
+  if (pid & kFlagBit) return;                          // corrupted: keeps the base
+  const int j = pid;
   const int wb = f.w / f.block;
   const int by = j / wb, bx = j - by * wb;
   const int rowb = f.block * f.c;                     // bytes per block row
@@ -117,42 +141,20 @@ decode_blocks_kernel(const nvrec_decode_job* __restrict__ jobs) {
   const uint8_t* ref = jr.reference;
   uint8_t* out = jr.plane;
   const int bs = f.block * f.block * f.c;
-  const int32_t br = jr.scratch[4 + j];
-
-  if (br < 0 || (br & kFlagBit)) {
-    // absent or corrupted block: reference content (P) or zero (I)
-    if (f.kind == 1 && ref == out) return;
-    if ((rowb & 15) == 0 && (pitch & 15) == 0 &&
-        ((reinterpret_cast<uintptr_t>(ref) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
-      const int per_row = rowb >> 4;
-      for (int q = lane; q < f.block * per_row; q += 32) {
-        const int y = q / per_row, x = q - y * per_row;
-        const size_t off = base + size_t(y) * pitch + 16 * size_t(x);
-        *reinterpret_cast<uint4*>(out + off) =
-            f.kind == 1 ? *reinterpret_cast<const uint4*>(ref + off) : make_uint4(0, 0, 0, 0);
-      }
-    } else {
-      for (int q = lane; q < bs; q += 32) {
-        const int y = q / rowb, x = q - y * rowb;
-        const size_t off = base + size_t(y) * pitch + x;
-        out[off] = f.kind == 1 ? ref[off] : 0;
-      }
-    }
-    return;
-  }
 
   // clean present block: decode its own payload range
   const uint8_t* offs = jr.mask.header + 14 + f.bitmap_len;
-  const int r = br;
   const int64_t s = lm::ld_u32le(offs + 4 * r);
   const int64_t e = block_end(f, offs, r);
   const int64_t avail = jr.mask.payload_received;     // len(enc.payload)
-  bool ok = bs <= kMaxBs && s < e && e <= avail && (e - s) % 3 == 0;
-  uint32_t* mk = sh_mark[warp];
+  bool ok = bs <= kMaxBs && s < e && e <= avail && (e - s) % 3 == 0 && e - s <= 3 * kMaxBs;
   if (ok) {
+    // the block's records in one round trip (all lanes' loads in flight)
+    const uint8_t* src = jr.payload + s;
+    for (int i = lane; i < int(e - s); i += 32) rec[i] = __ldg(src + i);
     for (int p = lane; p < bs; p += 32) mk[p] = 0;
     __syncwarp();
-    const uint8_t* pay = jr.payload + s;
+    const uint8_t* pay = rec;
     const int nrec = int((e - s) / 3);
     int pos = 0;                                       // samples so far
     for (int r0 = 0; r0 < nrec && pos <= bs; r0 += 32) {
@@ -200,13 +202,32 @@ decode_blocks_kernel(const nvrec_decode_job* __restrict__ jobs) {
     mk[p] = cur;
   }
   __syncwarp();
+  // one pixel (all channels) per lane step: samples are channel-planar
+  // (sample = ch * block^2 + y * block + x), pixels interleaved in the plane
   const int bb = f.block * f.block;
-  for (int q = lane; q < bs; q += 32) {
-    const int y = q / rowb, xb = q - y * rowb;
-    const int x = xb / f.c, ch = xb - x * f.c;
-    const uint32_t v = mk[ch * bb + y * f.block + x] & 0xFFFFu;
-    const size_t off = base + size_t(y) * pitch + xb;
-    out[off] = reconstruct(f.kind, v, f.quant, f.kind == 1 ? ref[off] : 0);
+  const int lg = f.block == 16 ? 4 : -1;             // shift instead of divide (16-px blocks)
+  for (int q = lane; q < bb; q += 32) {
+    const int y = lg > 0 ? q >> lg : q / f.block;
+    const int x = q - y * f.block;
+    const size_t off = base + size_t(y) * pitch + size_t(x) * f.c;
+    for (int ch = 0; ch < f.c; ++ch) {
+      const uint32_t v = mk[ch * bb + q] & 0xFFFFu;
+      out[off + ch] = reconstruct(f.kind, v, f.quant, f.kind == 1 ? ref[off + ch] : 0);
+    }
+  }
+}
+
+// Warps stride over the present ranks (grid sized for ~1/4 of the blocks).
+__global__ void __launch_bounds__(kThreads)
+decode_present_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  __shared__ uint32_t sh_mark[kWarps][kMaxBs];
+  __shared__ uint8_t sh_rec[kWarps][3 * kMaxBs];
+  const nvrec_decode_job& jr = jobs[blockIdx.y];
+  if (jr.mask.status[0] != 0) return;
+  const Fixed f = read_fixed(jr.mask.header);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * kWarps + warp; r < f.n_present; r += gridDim.x * kWarps) {
+    decode_one(jr, f, r, sh_mark[warp], sh_rec[warp], lane);
   }
 }
 
@@ -294,8 +315,9 @@ cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_bloc
                           cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
   decode_parse_kernel<<<n_jobs, kThreads, kParseStage, s>>>(jobs);
-  dim3 grid((max_blocks + kWarps - 1) / kWarps, n_jobs);
-  decode_blocks_kernel<<<grid, kThreads, 0, s>>>(jobs);
+  decode_copy_kernel<<<dim3((2 * 148 + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s>>>(jobs);
+  dim3 grid((max_blocks + 4 * kWarps - 1) / (4 * kWarps), n_jobs);
+  decode_present_kernel<<<grid, kThreads, 0, s>>>(jobs);
   decode_slow_kernel<<<n_jobs, 32, 0, s>>>(jobs);
   return cudaGetLastError();
 }

@@ -123,13 +123,15 @@ struct Header {
 // wire_bits and status exactly like nvrec_loss_mask.  When block_rank is
 // non-null it also receives, per block j, the present rank r of the block
 // (bit 30 set when flagged) or -1 for an absent block -- the index the
-// decoder needs to find the block's payload range.  Returns the status.
+// decoder needs to find the block's payload range -- and present_id the
+// inverse (present rank -> block, same flag bit).  Returns the status.
 // stage: optional shared-memory buffer (stage_cap bytes); when the header and
 // the received flags fit they are copied there once (one coalesced round
 // trip) and every later parse step reads shared memory.
 __device__ inline int lossmask_job(const nvrec_lossmask_job& job_in, int32_t* block_rank,
                                    Header* out_hdr, int* sh_scan /*[32]*/, int* sh_flagged,
-                                   uint8_t* stage = nullptr, int stage_cap = 0) {
+                                   uint8_t* stage = nullptr, int stage_cap = 0,
+                                   int32_t* present_id = nullptr) {
   nvrec_lossmask_job job = job_in;
   if (stage && job.header_len >= 0 && job.n_data >= 0 &&
       job.header_len + job.n_data <= stage_cap) {
@@ -214,6 +216,7 @@ __device__ inline int lossmask_job(const nvrec_lossmask_job& job_in, int32_t* bl
             }
             g = f ? 1 : 0;
             br = r | (f ? (1 << 30) : 0);
+            if (present_id) present_id[r] = j | (f ? (1 << 30) : 0);
           }
           ++r;
         }
