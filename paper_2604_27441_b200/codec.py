@@ -114,11 +114,14 @@ class DecodeBatch:
         self.max_blocks, self.max_shards, self.max_ranges = max_blocks, max_shards, max_ranges
         js = ctypes.sizeof(_native.DecodeJob)
         al = lambda n: (n + 255) // 256 * 256
+        # [jobs | headers | shard flags | ranges | payloads packed back to
+        # back]: the used prefix goes to the device in ONE copy
         self.o_hdr = al(js * max_jobs)
-        self.o_pay = self.o_hdr + al(max_jobs * max_header)
-        self.o_recv = self.o_pay + al(max_jobs * max_payload)
+        self.o_recv = self.o_hdr + al(max_jobs * max_header)
         self.o_rng = self.o_recv + al(max_jobs * max_shards)
-        self.in_bytes = self.o_rng + al(max_jobs * max_ranges * 16)
+        self.o_pay = self.o_rng + al(max_jobs * max_ranges * 16)
+        self.in_bytes = self.o_pay + al(max_jobs * (max_payload + 16))
+        self.used = self.o_pay
         self.host = torch.empty(self.in_bytes, dtype=torch.uint8, pin_memory=True)
         self.dev_in = torch.empty(self.in_bytes, dtype=torch.uint8, device=self.device)
         self.grid = torch.zeros((max_jobs, max_blocks), dtype=torch.uint8, device=self.device)
@@ -138,7 +141,7 @@ class DecodeBatch:
             raise ValueError("batch of %d frames exceeds capacity %d" % (len(items), self.max_jobs))
         hb = self.host.numpy()
         base = self.dev_in.data_ptr()
-        end = self.o_hdr
+        end_pay = self.o_pay
         self.headers = []
         for j, it in enumerate(items):
             hdr = bytes(it.header)
@@ -150,8 +153,9 @@ class DecodeBatch:
                 raise ValueError("frame %d exceeds range/shard capacity" % j)
             ho = self.o_hdr + j * self.max_header
             hb[ho:ho + len(hdr)] = np.frombuffer(hdr, np.uint8)
-            po = self.o_pay + j * self.max_payload
+            po = end_pay
             hb[po:po + pay.size] = pay
+            end_pay = po + (pay.size + 15) // 16 * 16
             ro = self.o_recv + j * self.max_shards
             if it.received is not None:
                 hb[ro:ro + it.n_data] = np.asarray(it.received, np.uint8)[:it.n_data]
@@ -178,18 +182,18 @@ class DecodeBatch:
             job.plane = it.out.data_ptr()
             job.plane_capacity = it.out.numel()
             job.scratch = self.scratch[j].data_ptr()
-            end = max(end, po + pay.size)
             self.headers.append(hdr)
         raw = bytes(self._jobs)[:ctypes.sizeof(_native.DecodeJob) * len(items)]
         hb[:len(raw)] = np.frombuffer(raw, np.uint8)
         self.n = len(items)
-        self.h2d_bytes = self.in_bytes
+        self.used = end_pay
+        self.h2d_bytes = self.used
 
     def launch(self, stream=None, copy: bool = True) -> None:
         s = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             if copy:
-                self.dev_in.copy_(self.host, non_blocking=True)
+                self.dev_in[:self.used].copy_(self.host[:self.used], non_blocking=True)
             _native.check(self.lib.nvrec_decode(ctypes.c_void_p(self.dev_in.data_ptr()),
                                                 self.n, self.max_blocks,
                                                 ctypes.c_void_p(int(s.cuda_stream))))

@@ -99,19 +99,12 @@ class ReceiverPipeline:
                                     body_len=len(body)))
         dec = self.dec[i]
         dec.stage(items)
-        self.bytes_in[i] = dec.o_pay + sum(len(f[1]) for f in frames)
+        self.bytes_in[i] = dec.used
         if self.step >= self.nbuf:
             self.s_h2d.wait_event(self.ev_cmp[i])       # staging buffer of step - nbuf read
         with torch.cuda.stream(self.s_h2d):
-            # descriptors + headers + bodies: copy only the used prefix of each
-            # job's region (the staging layout is job-strided)
-            dec.dev_in[:dec.o_pay].copy_(dec.host[:dec.o_pay], non_blocking=True)
-            for j, f in enumerate(frames):
-                lo = dec.o_pay + j * dec.max_payload
-                dec.dev_in[lo:lo + len(f[1])].copy_(dec.host[lo:lo + len(f[1])],
-                                                    non_blocking=True)
-            lo, hi = dec.o_recv, dec.in_bytes
-            dec.dev_in[lo:hi].copy_(dec.host[lo:hi], non_blocking=True)
+            # descriptors, headers, flags and the packed bodies: one copy
+            dec.dev_in[:dec.used].copy_(dec.host[:dec.used], non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
         self.s_cmp.wait_event(self.ev_h2d[i])
         if self.ev_slot[hd] is not None:
