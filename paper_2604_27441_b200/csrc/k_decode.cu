@@ -43,6 +43,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxBs = 768;               // 16 x 16 x 3 samples per block (fast path)
 constexpr int32_t kFlagBit = 1 << 30;
 constexpr int kParseStage = 40 * 1024;    // header + received flags staged in smem
+constexpr int kParseThreads = 1024;       // one bitmap byte per thread up to 8192 blocks
 
 struct Fixed {
   int kind, c, w, h, block, quant, n_present;
@@ -85,7 +86,7 @@ __device__ __forceinline__ int64_t block_end(const Fixed& f, const uint8_t* offs
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kParseThreads)
 decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
@@ -314,7 +315,7 @@ __global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
 cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_blocks,
                           cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  decode_parse_kernel<<<n_jobs, kThreads, kParseStage, s>>>(jobs);
+  decode_parse_kernel<<<n_jobs, kParseThreads, kParseStage, s>>>(jobs);
   decode_copy_kernel<<<dim3((2 * 148 + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s>>>(jobs);
   dim3 grid((max_blocks + 4 * kWarps - 1) / (4 * kWarps), n_jobs);
   decode_present_kernel<<<grid, kThreads, 0, s>>>(jobs);

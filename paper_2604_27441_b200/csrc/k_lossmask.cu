@@ -14,13 +14,13 @@
 namespace nvrec {
 
 namespace {
-constexpr int kThreads = 256;
+constexpr int kMaskThreads = 1024;   // one bitmap byte per thread up to 8192 blocks (1080p)
 using lm::block_exclusive_scan;
 }  // namespace
 
 constexpr int kStage = 40 * 1024;   // header + received flags staged in smem
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kMaskThreads)
 lossmask_kernel(const nvrec_lossmask_job* __restrict__ jobs) {
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
@@ -30,7 +30,7 @@ lossmask_kernel(const nvrec_lossmask_job* __restrict__ jobs) {
 }
 
 // Wire bitset (b, nbytes) -> ascending masked-patch list, rank table, count.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kMaskThreads)
 masklist_kernel(const uint8_t* __restrict__ bits, int nbytes, int ns,
                 int* __restrict__ list, int* __restrict__ rank, int* __restrict__ count) {
   __shared__ int sh_scan[32];
@@ -63,13 +63,13 @@ masklist_kernel(const uint8_t* __restrict__ bits, int nbytes, int ns,
 // ---------------------------------------------------------------------------
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  lossmask_kernel<<<n_jobs, kThreads, kStage, s>>>(jobs);
+  lossmask_kernel<<<n_jobs, kMaskThreads, kStage, s>>>(jobs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_masklist(const uint8_t* bits, int b, int nbytes, int ns, int* list,
                             int* rank, int* count, cudaStream_t s) {
-  masklist_kernel<<<b, kThreads, 0, s>>>(bits, nbytes, ns, list, rank, count);
+  masklist_kernel<<<b, kMaskThreads, 0, s>>>(bits, nbytes, ns, list, rank, count);
   return cudaGetLastError();
 }
 
