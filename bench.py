@@ -588,6 +588,9 @@ def main():
                       "serialised on one stream (separate pass)",
         "roofline": {"kernel": att_kind, "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "binding_unit": "mufu (SFU ex2): head_dim 32 gives 128 MMA-FLOP per "
+                                     "exponential, so the exp rate, not the tensor core, "
+                                     "bounds this kernel; see roofline.mufu.frac",
                      "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src,
                      "mufu": {"exp_per_s": exps / (att_ms / 1000.0) if att_ms else 0.0,
