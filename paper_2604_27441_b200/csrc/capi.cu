@@ -10,6 +10,16 @@
 
 #include "launch.cuh"
 
+#include <cstdlib>
+
+bool nvrec::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NVREC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 thread_local std::string g_err;

@@ -6,9 +6,58 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "nvrec_b200.h"
 
 namespace nvrec {
+
+// ---- programmatic dependent launch ---------------------------------------------------
+// Every kernel is launched by launch_pdl with programmatic stream serialisation:
+// its CTAs may be scheduled (and run their launch overhead) while the previous
+// kernel on the stream drains.  pdl_entry() is the first statement of every
+// kernel: it blocks until the predecessor grid has completed and its memory is
+// visible, then allows the successor to start launching.  Because every CTA
+// passes the wait before it can exit, completion stays transitive down the chain.
+// Heavy kernels (many waves of big CTAs) call pdl_wait() first and pdl_trigger()
+// only as they finish, so a light successor's CTAs are not parked on an SM
+// through the heavy kernel's last wave.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_entry() {
+  pdl_wait();
+  pdl_trigger();
+}
+bool pdl_enabled();   // NVREC_PDL=0 turns the attribute off (A/B, debugging)
+
+// Only light kernels (small CTAs, a few SMs' worth of resources) take the
+// attribute: a heavy successor launched early parks CTAs on every SM while it
+// waits, which starves the concurrent stream of the other modality (measured:
+// -2% step throughput when every launch used it).  Heavy kernels use
+// launch_seq, i.e. plain stream order; their pdl_entry() still releases light
+// successors early.
+template <bool kPdl = true, typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, A&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = kPdl && pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<P>(args)...);
+}
+template <typename... P, typename... A>
+inline cudaError_t launch_seq(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, A&&... args) {
+  return launch_pdl<false>(kernel, grid, block, smem, s, std::forward<A>(args)...);
+}
 
 constexpr int kMaxDim = 128;
 constexpr int kMaxNt = 16;

@@ -18,6 +18,7 @@ constexpr int kKeyTile = 64;
 template <int HD>
 __global__ void __launch_bounds__(128)
 attn_simt_kernel(AttnArgs a) {
+  pdl_entry();
   __shared__ __align__(16) float Ks[kKeyTile * HD];
   __shared__ __align__(16) float Vs[kKeyTile * HD];
   const int seq = blockIdx.y;
@@ -86,10 +87,10 @@ cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_
   dim3 grid(ceil_div(max_rows, 128), b * a.nt * a.heads);
   const int hd = a.d / a.heads;
   switch (hd) {
-    case 8: attn_simt_kernel<8><<<grid, 128, 0, s>>>(a); break;
-    case 16: attn_simt_kernel<16><<<grid, 128, 0, s>>>(a); break;
-    case 32: attn_simt_kernel<32><<<grid, 128, 0, s>>>(a); break;
-    case 64: attn_simt_kernel<64><<<grid, 128, 0, s>>>(a); break;
+    case 8: launch_seq(attn_simt_kernel<8>, grid, 128, 0, s, a); break;
+    case 16: launch_seq(attn_simt_kernel<16>, grid, 128, 0, s, a); break;
+    case 32: launch_seq(attn_simt_kernel<32>, grid, 128, 0, s, a); break;
+    case 64: launch_seq(attn_simt_kernel<64>, grid, 128, 0, s, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -468,6 +469,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
   if (kList && threadIdx.x == 0) a.redo_list[0] = 0;      // single fix-up CTA: re-arm
+  pdl_trigger();
 }
 
 // Merge the key-range partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(256)
 attn_combine_kernel(const float* __restrict__ part, float* __restrict__ ao,
                     const int* __restrict__ count, int seqs, int splits, int nt, int heads,
                     int ns, int d) {
+  pdl_entry();
   const int seq = blockIdx.y;
   const int b = seq / (nt * heads);
   const int nq = count ? count[b] : ns;
@@ -597,18 +600,18 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   dim3 grid(ta.groups * seqs * ta.splits);
   if (mode == 1 || !A.redo_list) {
     // exact maxima throughout (tests), or no fix-up list available
-    attn_tc_kernel<true, true, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+    launch_seq(attn_tc_kernel<true, true, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
   } else {
-    if (count) attn_tc_kernel<true, false, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
-    else attn_tc_kernel<false, false, false><<<grid, kThreads, smem, s>>>(tq, tk, tv, ta);
+    if (count) launch_seq(attn_tc_kernel<true, false, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
+    else launch_seq(attn_tc_kernel<false, false, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
     // exact fix-up of the (rare) items whose speculative exponent overflowed;
     // one CTA, exits at once when the list is empty, re-arms the list count
-    attn_tc_kernel<true, true, true><<<1, kThreads, smem, s>>>(tq, tk, tv, ta);
+    launch_pdl(attn_tc_kernel<true, true, true>, 1, kThreads, smem, s, tq, tk, tv, ta);
   }
   if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (ta.splits > 1 ? 1 : 0);
   if (ta.splits > 1) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
-    attn_combine_kernel<<<cg, 256, 0, s>>>(A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,
+    launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,
                                            A.ns, D.d);
   }
   return cudaGetLastError();

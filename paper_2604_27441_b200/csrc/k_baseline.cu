@@ -42,6 +42,7 @@ baseline_match_kernel(const uint8_t* __restrict__ planes, const uint8_t* __restr
                       const uint8_t* __restrict__ mask_bits, const int* __restrict__ list,
                       const int* __restrict__ count, uint8_t* __restrict__ out, int h, int w,
                       int ns, int nbytes) {
+  pdl_entry();
   __shared__ uint8_t win[kWin * kWin * C];
   __shared__ short ty[kB * kB], tx[kB * kB];
   __shared__ uint8_t tv[kB * kB * C];
@@ -148,6 +149,7 @@ baseline_match_kernel(const uint8_t* __restrict__ planes, const uint8_t* __restr
 // exclusive), all zero when nothing is masked
 __global__ void baseline_bbox_kernel(const int* __restrict__ list, const int* __restrict__ count,
                                      int ns, int gw, int h, int w, int* __restrict__ bbox) {
+  pdl_entry();
   const int b = blockIdx.x;
   int ymin = INT_MAX, ymax = -1, xmin = INT_MAX, xmax = -1;
   for (int r = threadIdx.x; r < count[b]; r += blockDim.x) {
@@ -193,6 +195,7 @@ __global__ void __launch_bounds__(kTile * kTile / 4)
 baseline_median_kernel(const uint8_t* __restrict__ base, const uint8_t* __restrict__ mask_bits,
                        const int* __restrict__ bbox, uint8_t* __restrict__ out, int h, int w,
                        int nbytes) {
+  pdl_entry();
   __shared__ uint8_t sv[kTile + 2][kTile + 2];     // block-match result, 1-px halo
   __shared__ uint8_t sm[kTile + 2][kTile + 2];     // mask, 1-px halo (0 outside the box)
   const int b = blockIdx.z;
@@ -254,15 +257,15 @@ cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t
   if (e != cudaSuccess) return e;
   dim3 grid(std::min(ns, 2 * 148), b);
   if (c == 3)
-    baseline_match_kernel<3><<<grid, 320, 0, s>>>(planes, refs, mask_bits, list, count,
+    launch_pdl(baseline_match_kernel<3>, grid, 320, 0, s, planes, refs, mask_bits, list, count,
                                                   match_out, h, w, ns, nbytes);
   else
-    baseline_match_kernel<1><<<grid, 320, 0, s>>>(planes, refs, mask_bits, list, count,
+    launch_pdl(baseline_match_kernel<1>, grid, 320, 0, s, planes, refs, mask_bits, list, count,
                                                   match_out, h, w, ns, nbytes);
   if ((e = cudaGetLastError()) != cudaSuccess || !depth) return e;
-  baseline_bbox_kernel<<<b, 32, 0, s>>>(list, count, ns, w / kB, h, w, bbox);
+  launch_pdl(baseline_bbox_kernel, b, 32, 0, s, list, count, ns, w / kB, h, w, bbox);
   dim3 mg(ceil_div(w, kTile), ceil_div(h, kTile), b);
-  baseline_median_kernel<<<mg, kTile * kTile / 4, 0, s>>>(base, mask_bits, bbox, out, h, w,
+  launch_pdl(baseline_median_kernel, mg, kTile * kTile / 4, 0, s, base, mask_bits, bbox, out, h, w,
                                                            nbytes);
   return cudaGetLastError();
 }

@@ -88,6 +88,7 @@ __device__ __forceinline__ int64_t block_end(const Fixed& f, const uint8_t* offs
 
 __global__ void __launch_bounds__(kParseThreads)
 decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  pdl_entry();
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
   extern __shared__ uint8_t stage[];
@@ -107,6 +108,7 @@ decode_parse_kernel(const nvrec_decode_job* __restrict__ jobs) {
 // where aligned; clean present blocks are overwritten by the next kernel.
 __global__ void __launch_bounds__(kThreads)
 decode_copy_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  pdl_entry();
   const nvrec_decode_job& jr = jobs[blockIdx.y];
   if (jr.mask.status[0] != 0) return;
   const Fixed f = read_fixed(jr.mask.header);
@@ -221,6 +223,7 @@ __device__ __forceinline__ void decode_one(const nvrec_decode_job& jr, const Fix
 // Warps stride over the present ranks (grid sized for ~1/4 of the blocks).
 __global__ void __launch_bounds__(kThreads)
 decode_present_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  pdl_entry();
   __shared__ uint32_t sh_mark[kWarps][kMaxBs];
   __shared__ uint8_t sh_rec[kWarps][3 * kMaxBs];
   const nvrec_decode_job& jr = jobs[blockIdx.y];
@@ -234,6 +237,7 @@ decode_present_kernel(const nvrec_decode_job* __restrict__ jobs) {
 
 // Literal replay of codec.py:283-317 for frames the fast path rejected.
 __global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  pdl_entry();
   const nvrec_decode_job& jr = jobs[blockIdx.x];
   if (threadIdx.x != 0 || jr.mask.status[0] != 0 || jr.scratch[0] == 0) return;
   const Fixed f = read_fixed(jr.mask.header);
@@ -315,11 +319,11 @@ __global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
 cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_blocks,
                           cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  decode_parse_kernel<<<n_jobs, kParseThreads, kParseStage, s>>>(jobs);
-  decode_copy_kernel<<<dim3((2 * 148 + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s>>>(jobs);
+  launch_pdl(decode_parse_kernel, n_jobs, kParseThreads, kParseStage, s, jobs);
+  launch_pdl(decode_copy_kernel, dim3((2 * 148 + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s, jobs);
   dim3 grid((max_blocks + 4 * kWarps - 1) / (4 * kWarps), n_jobs);
-  decode_present_kernel<<<grid, kThreads, 0, s>>>(jobs);
-  decode_slow_kernel<<<n_jobs, 32, 0, s>>>(jobs);
+  launch_pdl(decode_present_kernel, grid, kThreads, 0, s, jobs);
+  launch_pdl(decode_slow_kernel, n_jobs, 32, 0, s, jobs);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ constexpr int kEmbThreads = 256;
 template <bool U8>
 __global__ void __launch_bounds__(kEmbThreads)
 embed_kernel(EmbedArgs a) {
+  pdl_entry();
   extern __shared__ float smem[];
   const Dims& D = a.D;
   const int kc_max = D.p * D.c > D.p ? D.p * D.c : D.p;
@@ -162,6 +163,7 @@ constexpr int kLnTok = 32;
 
 __global__ void __launch_bounds__(256)
 ln_qkv_kernel(LnQkvArgs a) {
+  pdl_entry();
   extern __shared__ float smem[];
   const int d = a.D.d;
   float* Xs = smem;               // [kLnTok][d]
@@ -183,6 +185,7 @@ ln_qkv_kernel(LnQkvArgs a) {
 __global__ void copy_plane_kernel(const uint8_t* __restrict__ frames,
                                   const int32_t* __restrict__ frame_index, int F,
                                   size_t frame_bytes, uint8_t* __restrict__ out) {
+  pdl_entry();
   const int b = blockIdx.y;
   const uint4* src = reinterpret_cast<const uint4*>(
       frames + size_t(frame_index[b * F + F - 1]) * frame_bytes);
@@ -204,10 +207,10 @@ cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s) {
   size_t smem = embed_smem_bytes(a.D);
   if (u8) {
     cudaFuncSetAttribute(embed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    embed_kernel<true><<<grid, kEmbThreads, smem, s>>>(a);
+    launch_seq(embed_kernel<true>, grid, kEmbThreads, smem, s, a);
   } else {
     cudaFuncSetAttribute(embed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    embed_kernel<false><<<grid, kEmbThreads, smem, s>>>(a);
+    launch_seq(embed_kernel<false>, grid, kEmbThreads, smem, s, a);
   }
   return cudaGetLastError();
 }
@@ -215,7 +218,7 @@ cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s) {
 cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s) {
   dim3 grid(ceil_div(a.ns, kLnTok), a.D.nt, b);
   size_t smem = sizeof(float) * 2 * kLnTok * a.D.d;
-  ln_qkv_kernel<<<grid, 256, smem, s>>>(a);
+  launch_seq(ln_qkv_kernel, grid, 256, smem, s, a);
   return cudaGetLastError();
 }
 
@@ -223,7 +226,7 @@ cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index,
                               size_t frame_bytes, uint8_t* out, int b, cudaStream_t s) {
   int blocks = int((frame_bytes / 16 + 255) / 256);
   if (blocks > 148 * 4) blocks = 148 * 4;
-  copy_plane_kernel<<<dim3(blocks, b), 256, 0, s>>>(frames, frame_index, F, frame_bytes, out);
+  launch_pdl(copy_plane_kernel, dim3(blocks, b), 256, 0, s, frames, frame_index, F, frame_bytes, out);
   return cudaGetLastError();
 }
 

@@ -77,6 +77,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
 template <int C>
 __global__ void __launch_bounds__(kThreads, 1)
 embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tcw) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using S = EmbSmem<C>;
   // pointer arithmetic (not integer casts) keeps the shared address space
@@ -294,6 +295,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<256>(tmem);
+  pdl_trigger();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -333,7 +335,7 @@ cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int tiles = ((a.nh + kTh - 1) / kTh) * ((a.nw + kTw - 1) / kTw);
-  embed_tc_kernel<C><<<dim3(tiles, a.D.nt, a.b), kThreads, smem, s>>>(tm, a, *a.tcw);
+  launch_seq(embed_tc_kernel<C>, dim3(tiles, a.D.nt, a.b), kThreads, smem, s, tm, a, *a.tcw);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ constexpr int kStage = 40 * 1024;   // header + received flags staged in smem
 
 __global__ void __launch_bounds__(kMaskThreads)
 lossmask_kernel(const nvrec_lossmask_job* __restrict__ jobs) {
+  pdl_entry();
   __shared__ int sh_scan[32];
   __shared__ int sh_flagged;
   extern __shared__ uint8_t stage[];
@@ -33,6 +34,7 @@ lossmask_kernel(const nvrec_lossmask_job* __restrict__ jobs) {
 __global__ void __launch_bounds__(kMaskThreads)
 masklist_kernel(const uint8_t* __restrict__ bits, int nbytes, int ns,
                 int* __restrict__ list, int* __restrict__ rank, int* __restrict__ count) {
+  pdl_entry();
   __shared__ int sh_scan[32];
   const int b = blockIdx.x;
   const uint8_t* mb = bits + size_t(b) * nbytes;
@@ -63,13 +65,13 @@ masklist_kernel(const uint8_t* __restrict__ bits, int nbytes, int ns,
 // ---------------------------------------------------------------------------
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
-  lossmask_kernel<<<n_jobs, kMaskThreads, kStage, s>>>(jobs);
+  launch_pdl(lossmask_kernel, n_jobs, kMaskThreads, kStage, s, jobs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_masklist(const uint8_t* bits, int b, int nbytes, int ns, int* list,
                             int* rank, int* count, cudaStream_t s) {
-  masklist_kernel<<<b, kMaskThreads, 0, s>>>(bits, nbytes, ns, list, rank, count);
+  launch_pdl(masklist_kernel, b, kMaskThreads, 0, s, bits, nbytes, ns, list, rank, count);
   return cudaGetLastError();
 }
 

@@ -136,6 +136,7 @@ __device__ __forceinline__ uint32_t xtime4(uint32_t w) {
 template <bool kWord>
 __global__ void __launch_bounds__(kThreads)
 rs_kernel(const nvrec_rs_job* __restrict__ jobs) {
+  pdl_entry();
   extern __shared__ uint8_t sh_coef[];
   const nvrec_rs_job& jb = jobs[blockIdx.y];
   const int n = jb.n, m = jb.m, L = jb.shard_len;
@@ -249,8 +250,8 @@ cudaError_t launch_rs(const nvrec_rs_job* jobs, int n_jobs, int max_shard_len, i
     cudaFuncSetAttribute(rs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxCoef + 16);
     attr = true;
   }
-  if (word) rs_kernel<true><<<grid, kThreads, smem, s>>>(jobs);
-  else rs_kernel<false><<<grid, kThreads, smem, s>>>(jobs);
+  if (word) launch_pdl(rs_kernel<true>, grid, kThreads, smem, s, jobs);
+  else launch_pdl(rs_kernel<false>, grid, kThreads, smem, s, jobs);
   return cudaGetLastError();
 }
 

@@ -158,6 +158,7 @@ __device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, in
 template <bool kNarrow>
 __global__ void __launch_bounds__(256)
 token_kernel(TokenArgs a) {
+  pdl_wait();
   extern __shared__ float smem[];
   __shared__ int spos[48];
   const int b = blockIdx.y;
@@ -166,6 +167,7 @@ token_kernel(TokenArgs a) {
     token_tile<kNarrow>(a, b, r0, cnt, smem, spos);
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 size_t token_smem_bytes(const Dims& D, int P) {
@@ -185,10 +187,10 @@ cudaError_t launch_token(const TokenArgs& a_in, int b, int max_rows, cudaStream_
   if (narrow) grid.x = std::min<int>(grid.x, std::max(1, 2 * 148 / b));
   if (narrow) {
     cudaFuncSetAttribute(token_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    token_kernel<true><<<grid, 256, smem, s>>>(a);
+    launch_seq(token_kernel<true>, grid, 256, smem, s, a);
   } else {
     cudaFuncSetAttribute(token_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    token_kernel<false><<<grid, 256, smem, s>>>(a);
+    launch_seq(token_kernel<false>, grid, 256, smem, s, a);
   }
   return cudaGetLastError();
 }

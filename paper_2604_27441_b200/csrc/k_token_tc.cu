@@ -78,6 +78,7 @@ __device__ __forceinline__ void layernorm64(const float* x, float* y, const floa
 
 __global__ void __launch_bounds__(kThreads, 1)
 token_tc_kernel(TokenTcArgs a) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   // pointer arithmetic (not integer casts) keeps the shared address space
   TokSmem& sm = *reinterpret_cast<TokSmem*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
@@ -320,6 +321,7 @@ token_tc_kernel(TokenTcArgs a) {
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(sm.tmem_base);
+  pdl_trigger();
 }
 
 }  // namespace
@@ -344,7 +346,7 @@ cudaError_t launch_token_tc(const TokenTcArgs& a, cudaStream_t s) {
   const int P = 4 * (32 / a.nt);
   const int tiles = ((a.ns + P - 1) / P) * a.b;
   const int ctas = (tiles + kSlots - 1) / kSlots;
-  token_tc_kernel<<<ctas < sms ? ctas : sms, kThreads, smem, s>>>(a);
+  launch_seq(token_tc_kernel, ctas < sms ? ctas : sms, kThreads, smem, s, a);
   return cudaGetLastError();
 }
 
