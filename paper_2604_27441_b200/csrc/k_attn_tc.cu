@@ -289,6 +289,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
 #pragma unroll
       for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
       const int jend = t < ntq ? nkv : 0;          // idle warpgroup: no live rows
+      // a warp whose 32 query rows are all past the stream's queries (the
+      // tail of the last group; most warps of a pruned launch) keeps the
+      // barrier protocol but skips the exponentials -- rows are independent
+      // in the MMAs, so its stale P/O rows are never read back
+      const bool rows_live = q0 + t * kTileQ + quarter * 32 < nq;
       const int gst = gs[t];
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
       // the key-tile loop, specialised for speculative / exact maxima
@@ -310,7 +315,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           // more than kSlack (P > 2^kSlack) rescales its stored P by an exact
           // power of two.  Softmax is shift-invariant, so this is the same sum.
           float mn = m;
-          if (j == 0 || EX) {
+          if ((j == 0 || EX) && rows_live) {
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -332,6 +337,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           const float2 nm2 = make_float2(-mn, -mn);
   #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
+            if (rows_live) {
             uint32_t r[64], pk[32];
             tmem_ld32(t_s + 64 * h2, r);
             tmem_ld32(t_s + 64 * h2 + 32, r + 32);
@@ -352,6 +358,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             }
             tmem_st16(t_s + 32 * h2, pk);
             tmem_st16(t_s + 32 * h2 + 16, pk + 16);
+            }
             if (h2 == 0 && j > 0) {
               mbar_wait(&sm.pv_full[t], (g - 1) & 1);
               tc_fence_after();
