@@ -5,7 +5,7 @@
 //
 // CTA = 128 tokens = an 8 x 16 rectangle of patches of one (stream, time
 // slice); 6 warps:
-//   warp 4     producer: per K stage (tubelet frame tt, 2 patch rows) one 5-D
+//   warp 4     producer: per K stage (tubelet frame tt, kPy patch rows) one 5-D
 //              TMA box of raw u8 pixels [8 ih][2 py][16 iw][16*c bytes]
 //              straight from the HWC planes (zero-filled past the frame edge)
 //              and one bulk copy of the stage's fp16 weight block
@@ -39,14 +39,18 @@ constexpr int kThreads = 192;
 // RGB: two CTAs per SM (<= ~113 KB of shared memory each), so one CTA's
 // epilogue and qkv GEMM overlap the other's pixel stream; the qkv weights
 // reuse the A ring and the LN output reuses the raw-pixel ring once the K loop
-// is done.  Depth (c = 1) has small stages: deeper rings, same sharing.
+// is done.  A K stage is kPy patch rows of one tubelet frame: 2 for RGB
+// (K = 96), 4 for depth (K = 64) so a depth stage is not dominated by its
+// barrier round trip.
 template <int C>
 struct __align__(128) EmbSmem {
+  static constexpr int kPy = C == 3 ? 2 : 4;                 // patch rows per K stage
+  static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame
   static constexpr int kNst = C == 3 ? 2 : 3;                // A/W (MMA operand) ring
-  static constexpr int kNu8 = C == 3 ? 3 : 6;                // raw-pixel TMA ring
-  static constexpr uint32_t kU8 = kTh * 2 * kTw * 16 * C;   // raw pixels per stage
-  static constexpr uint32_t kA = kRows * 32 * C * 2;        // fp16 A per stage
-  static constexpr uint32_t kW = 64 * 32 * C * 2;           // fp16 W per stage
+  static constexpr int kNu8 = C == 3 ? 3 : 4;                // raw-pixel TMA ring
+  static constexpr uint32_t kU8 = kTh * kPy * kTw * 16 * C; // raw pixels per stage
+  static constexpr uint32_t kA = kRows * 16 * kPy * C * 2;  // fp16 A per stage
+  static constexpr uint32_t kW = 64 * 16 * kPy * C * 2;     // fp16 W per stage
   static constexpr uint32_t kQkvW = 192 * 64 * 2, kA2 = kRows * 64 * 2;
   static constexpr uint32_t kARegion = kNst * kA > kQkvW ? kNst * kA : kQkvW;
   static constexpr uint32_t kURegion = kNu8 * kU8 > kA2 ? kNu8 * kU8 : kA2;
@@ -86,7 +90,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   const int tiles_w = (a.nw + kTw - 1) / kTw;
   const int ih0 = (blockIdx.x / tiles_w) * kTh, iw0 = (blockIdx.x % tiles_w) * kTw;
   const int it = blockIdx.y, b = blockIdx.z;
-  const int T = a.D.T, nst = T * 8;
+  const int T = a.D.T, nst = T * S::kSpt;
 
   if (warp == 4 && lane == 0) {
     for (int i = 0; i < S::kNu8; ++i) {
@@ -129,8 +133,8 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         const int pu = st % S::kNu8;
         mbar_wait(&sm.u8_empty[pu], ((st / S::kNu8) & 1) ^ 1);
         mbar_expect_tx(&sm.u8_full[pu], S::kU8);
-        tma_load_5d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], 0, iw0, 2 * (st % 8), ih0,
-                    sm.slot[st / 8]);
+        tma_load_5d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], 0, iw0, S::kPy * (st % S::kSpt), ih0,
+                    sm.slot[st / S::kSpt]);
       }
     } else if (lane == 1) {
       // weights follow the MMA-operand ring (independent thread, own waits)
@@ -138,7 +142,9 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         const int ps = st % S::kNst;
         mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);
         mbar_expect_tx(&sm.w_full[ps], S::kW);
-        bulk_load(sm.w[ps], tcw.emb + size_t(st) * tcw.emb_stage_elems, S::kW, &sm.w_full[ps]);
+        // the host packs 2-row stages back to back, so kPy/2 of them are one block
+        bulk_load(sm.w[ps], tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems, S::kW,
+                  &sm.w_full[ps]);
       }
       // qkv weights into the A ring once the last embed MMA has read it
       mbar_wait(&sm.acc_full, 0);
@@ -156,7 +162,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         tc_fence_after();
         const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w[ps]);
 #pragma unroll
-        for (int kk = 0; kk < 2 * C; ++kk)
+        for (int kk = 0; kk < S::kPy * C; ++kk)
           mma_ss(tmem, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
                  sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
         mma_commit(&sm.empty[ps]);
@@ -185,12 +191,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       const int ps = st % S::kNst, pu = st % S::kNu8;
       mbar_wait(&sm.u8_full[pu], (st / S::kNu8) & 1);
       if (st >= S::kNst) mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);   // A slot drained
-      const bool zero = last_slice && (st / 8) == T - 1 && masked;   // corrupted frame
+      const bool zero = last_slice && (st / S::kSpt) == T - 1 && masked;   // corrupted frame
       uint8_t* arow = sm.a(ps) + m * 16;
 #pragma unroll
-      for (int pyl = 0; pyl < 2; ++pyl) {
+      for (int pyl = 0; pyl < S::kPy; ++pyl) {
         const uint4* src =
-            reinterpret_cast<const uint4*>(sm.u8(pu) + ((ihl * 2 + pyl) * kTw + iwl) * 16 * C);
+            reinterpret_cast<const uint4*>(sm.u8(pu) + ((ihl * S::kPy + pyl) * kTw + iwl) * 16 * C);
 #pragma unroll
         for (int q = 0; q < C; ++q) {
           uint4 v = zero ? make_uint4(0, 0, 0, 0) : src[q];
@@ -321,7 +327,7 @@ cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
                         cuuint64_t(a.n_slots)};
   cuuint64_t strides[4] = {cuuint64_t(16 * C), cuuint64_t(a.w) * C, cuuint64_t(16) * a.w * C,
                            cuuint64_t(a.h) * a.w * C};
-  cuuint32_t box[5] = {cuuint32_t(16 * C), kTw, 2, kTh, 1};
+  cuuint32_t box[5] = {cuuint32_t(16 * C), kTw, EmbSmem<C>::kPy, kTh, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(a.frames), dims, strides,
          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
