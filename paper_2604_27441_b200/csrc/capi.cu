@@ -158,9 +158,10 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
     L.vth = take(seqrows * 2);
     L.q = L.k = L.v = SIZE_MAX;
     L.part = take(size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads * ns * 36 * 4);
-    // work items: query groups x splits x sequences (+ the count)
+    // work items: query groups (>= one 128-query tile) x splits x sequences
+    // (+ the count)
     L.redo = take((1 + size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads *
-                   ((ns + 2 * nvrec::kAttnQTile - 1) / (2 * nvrec::kAttnQTile))) * 4);
+                   ((ns + nvrec::kAttnQTile - 1) / nvrec::kAttnQTile)) * 4);
   } else {
     L.q = take(seqrows * 4);
     L.k = take(seqrows * 4);

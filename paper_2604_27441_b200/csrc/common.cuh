@@ -130,7 +130,7 @@ struct Act {
   int* redo_list;    // bf16 path: [0] count + attention work items for the exact fix-up
   int b, ns, nh, nw, ns_pad;
 };
-constexpr int kAttnMaxSplits = 3;
+constexpr int kAttnMaxSplits = 6;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -48,12 +48,17 @@ constexpr int kHd = 32;
 constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
 constexpr int kStages = 6;
-constexpr int kQT = 2;                                 // query tiles per CTA
-constexpr int kThreads = (4 * kQT + 4) * 32;           // softmax WGs + (TMA, MMA, 2 idle)
-// Register split (setmaxnreg): the launch gives every thread 168 registers
-// (3 warps per SMSP); the TMA/MMA warpgroup drops to kRegsCtl and the two
-// softmax warpgroups rise to kRegsSoftmax (kRegsCtl + 2 kRegsSoftmax <= 512).
-constexpr int kRegsCtl = 40, kRegsSoftmax = 232;
+// QT = query tiles per CTA: 2 for dense launches (one CTA per SM, all 512 TMEM
+// columns); 1 for pruned launches (a handful of masked-patch queries per
+// sequence: latency-bound, so two CTAs share an SM and the key range is split
+// twice as finely).
+__host__ __device__ constexpr int threads_for(int QT) { return (4 * QT + 4) * 32; }
+// Register split (setmaxnreg): QT = 2 launches 168 registers per thread (3
+// warps per SMSP), QT = 1 launches 128 (two CTAs, 4 warps per SMSP); the
+// TMA/MMA warpgroup drops to kRegsCtl and the softmax warpgroups rise to
+// regs_softmax (per SMSP: ctl + softmax warps x registers <= 512).
+constexpr int kRegsCtl = 40;
+__host__ __device__ constexpr int regs_softmax(int QT) { return QT == 2 ? 232 : 216; }
 constexpr int kPolyOf4 = 1;                            // FMA-pipe exp2 pairs per 4
 constexpr uint32_t kQBytes = kTileQ * kHd * 2;         // 8 KB
 constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
@@ -62,15 +67,16 @@ constexpr uint32_t kIdescS = idesc_bf16(128, 128);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
 constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buffer
 constexpr float kSlackSum = 256.f;                     // speculative-max headroom: row sum of P
-static_assert(kQT * 2 * kTileK <= 512, "TMEM budget");
+static_assert(2 * 2 * kTileK <= 512, "TMEM budget");
 
+template <int QT>
 struct __align__(1024) Smem {
   uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
-  uint8_t q[kQT][kQBytes];          // 512-aligned (SWIZZLE_64B atoms)
+  uint8_t q[QT][kQBytes];           // 512-aligned (SWIZZLE_64B atoms)
   uint8_t k[kStages][kKBytes];
   uint64_t q_full;
   uint64_t kv_full[kStages], kv_empty[kStages];
-  uint64_t s_full[kQT][2], p_full[kQT], pv_full[kQT], o_read[kQT], done;
+  uint64_t s_full[QT][2], p_full[QT], pv_full[QT], o_read[QT], done;
   int redo[3];                      // per group iteration (mod 3): speculative max overflowed
   uint32_t tmem_base;
 };
@@ -97,14 +103,14 @@ __device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 *
 // kExact: exact per-tile maxima (the fix-up); otherwise the speculative
 // running max, and a CTA whose exponent overflowed records its item for the
 // fix-up launch that follows on the same stream.
-template <bool kMulti, bool kExact, bool kList>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kMulti, bool kExact, bool kList, int kQT>
+__global__ void __launch_bounds__(threads_for(kQT), kQT == 1 ? 2 : 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
   pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
+  Smem<kQT>& sm = *reinterpret_cast<Smem<kQT>*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv_all = (a.ns + kTileK - 1) / kTileK;
   const int n_list = kList ? a.redo_list[0] : 0;
@@ -153,7 +159,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
   }
-  if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
+  if (warp == 0) tmem_alloc<kQT * 256>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -266,7 +272,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
   }
   } else {
-    setmaxnreg_inc<kRegsSoftmax>();
+    setmaxnreg_inc<regs_softmax(kQT)>();
   for (int kit = 0;; ++kit) {
     const int it = item_at(kit);
     if (it < 0) break;
@@ -474,7 +480,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == 0) tmem_dealloc<kQT * 256>(tmem);
   if (kList && threadIdx.x == 0) a.redo_list[0] = 0;      // single fix-up CTA: re-arm
   pdl_trigger();
 }
@@ -562,32 +568,34 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.d = D.d;
   ta.seqs = seqs;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
-  const size_t smem = sizeof(Smem) + 1024;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(attn_tc_kernel<false, false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(attn_tc_kernel<true, false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int s2 = int(sizeof(Smem<2>) + 1024), s1 = int(sizeof(Smem<1>) + 1024);
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaFuncSetAttribute(attn_tc_kernel<false, false, false, 2>, attr, s2);
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, false, 2>, attr, s2);
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, true, 2>, attr, s2);
+    cudaFuncSetAttribute(attn_tc_kernel<true, false, false, 1>, attr, s1);
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, false, 1>, attr, s1);
+    cudaFuncSetAttribute(attn_tc_kernel<true, true, true, 1>, attr, s1);
   }
-  // One CTA per SM (TMEM).  A pruned launch (compact masked-patch queries,
-  // count on the device) is sized for one query group per sequence and loops
-  // over further groups; a short grid splits the key range instead
-  // (flash-decoding partials merged by attn_combine_kernel) so every SM works.
+  // Dense launch: two query tiles per CTA, one CTA per SM (all of TMEM).  A
+  // pruned launch (compact masked-patch queries, count on the device): one
+  // query tile per CTA, two CTAs per SM, sized for one query group per
+  // sequence and looping over further groups.  A short grid splits the key
+  // range (flash-decoding partials merged by attn_combine_kernel) so every
+  // SM slot works.
+  const int qt = count ? 1 : 2, per_sm = count ? 2 : 1;
   const int nkv = ceil_div(A.ns, kTileK);
-  ta.groups = count ? 1 : ceil_div(A.ns, kQT * kTileQ);
+  ta.groups = count ? 1 : ceil_div(A.ns, qt * kTileQ);
   int best = 1;
   double best_t = 1e30;
   for (int sp = 1; sp <= kAttnMaxSplits && sp <= nkv && A.part; ++sp) {
     const int ctas = ta.groups * seqs * sp;
-    const double t = double(ceil_div(ctas, sms)) / sp + (sp > 1 ? 0.05 : 0.0);
+    const double t = double(ceil_div(ctas, per_sm * sms)) / sp + (sp > 1 ? 0.05 : 0.0);
     if (t < best_t - 1e-9) { best_t = t; best = sp; }
   }
   static int force = -2;
@@ -604,22 +612,29 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   }
   ta.mode = mode;
   ta.redo_list = A.redo_list;
-  dim3 grid(ta.groups * seqs * ta.splits);
-  if (mode == 1 || !A.redo_list) {
-    // exact maxima throughout (tests), or no fix-up list available
-    launch_seq(attn_tc_kernel<true, true, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
-  } else {
-    if (count) launch_seq(attn_tc_kernel<true, false, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
-    else launch_seq(attn_tc_kernel<false, false, false>, grid, kThreads, smem, s, tq, tk, tv, ta);
-    // exact fix-up of the (rare) items whose speculative exponent overflowed;
-    // one CTA, exits at once when the list is empty, re-arms the list count
-    launch_pdl(attn_tc_kernel<true, true, true>, 1, kThreads, smem, s, tq, tk, tv, ta);
-  }
+  const dim3 grid(ta.groups * seqs * ta.splits);
+  auto run = [&](auto qt_tag) {
+    constexpr int QT = decltype(qt_tag)::value;
+    const int nth = threads_for(QT);
+    const size_t smem = sizeof(Smem<QT>) + 1024;
+    if (mode == 1 || !A.redo_list) {
+      // exact maxima throughout (tests), or no fix-up list available
+      launch_seq(attn_tc_kernel<true, true, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
+    } else {
+      if constexpr (QT == 1) launch_seq(attn_tc_kernel<true, false, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
+      else launch_seq(attn_tc_kernel<false, false, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
+      // exact fix-up of the (rare) items whose speculative exponent overflowed;
+      // one CTA, exits at once when the list is empty, re-arms the list count
+      launch_pdl(attn_tc_kernel<true, true, true, QT>, 1, nth, smem, s, tq, tk, tv, ta);
+    }
+  };
+  if (qt == 1) run(std::integral_constant<int, 1>{});
+  else run(std::integral_constant<int, 2>{});
   if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (ta.splits > 1 ? 1 : 0);
   if (ta.splits > 1) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
-    launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt, D.heads,
-                                           A.ns, D.d);
+    launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt,
+               D.heads, A.ns, D.d);
   }
   return cudaGetLastError();
 }
