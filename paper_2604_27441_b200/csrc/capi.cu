@@ -217,10 +217,13 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     const bool prune_here = last && pruned;
     // block li's spatial attention: Q/K/V were written by the previous stage
     cudaError_t e;
+    int splits = 1;
     if (fast) {
       ProfScope ps(NVREC_STAGE_ATTN_TC, s);
       int nk = 1;
-      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk);
+      // the SIMT token kernel (last block) merges key-split partials itself
+      const bool defer = last || !nvrec::token_tc_supported(D) || !m->W.tc.blk[li];
+      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits);
       ps.kernels(nk);
     } else {
       nvrec::AttnArgs aa{};
@@ -242,6 +245,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     ta.list = prune_here ? A.list : nullptr;
     ta.count = A.count;
     ta.x = A.x; ta.ao = A.ao;
+    ta.part = A.part; ta.splits = splits;
     ta.dst = dst;
     // the next block is the last: its Q rows are compact when pruned
     ta.dst.rank = (!last && li + 1 == D.layers - 1 && pruned) ? A.rank : nullptr;

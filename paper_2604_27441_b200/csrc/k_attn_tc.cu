@@ -545,7 +545,7 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
-                           int* n_kernels) {
+                           int* n_kernels, bool defer_combine, int* splits_out) {
   const int seqs = A.b * D.nt * D.heads;
   CUtensorMap tq, tk, tv;
   const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
@@ -630,8 +630,10 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   };
   if (qt == 1) run(std::integral_constant<int, 1>{});
   else run(std::integral_constant<int, 2>{});
-  if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (ta.splits > 1 ? 1 : 0);
-  if (ta.splits > 1) {
+  const bool combine = ta.splits > 1 && !defer_combine;
+  if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (combine ? 1 : 0);
+  if (splits_out) *splits_out = ta.splits;
+  if (combine) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
     launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt,
                D.heads, A.ns, D.d);

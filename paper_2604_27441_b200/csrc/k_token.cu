@@ -50,7 +50,27 @@ __device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, in
     const int j = t / nt, it = t - j * nt;
     const size_t slice = size_t(b * nt + it) * a.ns;
     Xs[i] = a.x[(slice + spos[j]) * d + o];
-    As[i] = a.ao[(slice + r0 + j) * d + o];
+    if (a.splits > 1) {
+      // merge the key-range partials of this row and head (attn_combine_kernel's
+      // O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), fused into the load)
+      const int hh = o / D.hd, e = o - hh * D.hd;
+      const size_t seqs = size_t(gridDim.y) * nt * D.heads;
+      const size_t seq = size_t(b * nt + it) * D.heads + hh;
+      const float* p0 = a.part + (seq * a.ns + r0 + j) * 36;
+      const size_t sstride = seqs * a.ns * 36;
+      float M = -INFINITY;
+      for (int sp = 0; sp < a.splits; ++sp) M = fmaxf(M, __ldg(p0 + sp * sstride + 32));
+      float acc = 0.f, L = 0.f;
+      for (int sp = 0; sp < a.splits; ++sp) {
+        const float* p = p0 + sp * sstride;
+        const float wgt = exp2f(__ldg(p + 32) - M);
+        L = fmaf(__ldg(p + 33), wgt, L);
+        acc = fmaf(__ldg(p + e), wgt, acc);
+      }
+      As[i] = acc / L;
+    } else {
+      As[i] = a.ao[(slice + r0 + j) * d + o];
+    }
   }
   __syncthreads();
 

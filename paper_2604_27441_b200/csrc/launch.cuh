@@ -45,6 +45,8 @@ struct TokenArgs {
   const int* count;
   float* x;             // [b][nt][ns][d]
   const float* ao;      // [b][nt][ns][d], row r (compact when list)
+  const float* part;    // or: key-split attention partials [split][seq][ns][36] to
+  int splits;           //     merge on load (splits > 1; the combine kernel is skipped)
   QkvDst dst;           // next block's Q/K/V
   int img_h, img_w, nh, nw, ns;
   float* out_f32;       // (b, c, h, w) or null
@@ -98,8 +100,11 @@ cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index,
                               size_t frame_bytes, uint8_t* out, int b, cudaStream_t s);
 cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_t s);
+// defer_combine: the consumer merges key-split partials itself (token_kernel);
+// *splits_out receives the split count (1 = ao written directly)
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
-                           int* n_kernels = nullptr);
+                           int* n_kernels = nullptr, bool defer_combine = false,
+                           int* splits_out = nullptr);
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
