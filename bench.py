@@ -171,13 +171,16 @@ class ModalityWork:
             buf.copy_(self.host_planes)           # the decoder writes planes here
 
     def device_step(self, stream):
-        """Loss mask + recovery with inputs resident in HBM."""
+        """Loss mask + recovery with inputs resident in HBM, merged in place
+        (the serving mode of RecoveryPipeline: the recovered patches land in
+        the corrupted plane's slot; the model never reads those pixels, so
+        repeating the step recomputes the same plane)."""
         from paper_2604_27441_b200 import _native
         import ctypes
         _native.check(self.lm.lib.nvrec_loss_mask(ctypes.c_void_p(self.lm.dev_in.data_ptr()),
                                                   self.lm.n,
                                                   ctypes.c_void_p(int(stream.cuda_stream))))
-        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+        self.engine.recover_device(self.frames, self.index, self.lm.wire, in_place=True)
 
     def e2e_step(self, stream):
         """Streaming in-process backend through pinned host buffers: the

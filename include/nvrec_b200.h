@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define NVREC_ABI_VERSION 2
+#define NVREC_ABI_VERSION 3
 
 enum {
   NVREC_OK = 0,
@@ -105,7 +105,10 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b,
  * out: u8 (b, h, w, c) merged planes (unmasked pixels = corrupted plane).
  * Only masked patches are decoded (exact: the merge discards the rest).
  * The stacked frames are read before `out` is written, so `out` may alias
- * the planes of one reference slot (in-place ring update). */
+ * the planes of one reference slot (in-place ring update).  out == NULL merges
+ * in place: each stream's corrupted plane (slot frame_index[b*F + F-1], which
+ * must then be writable) receives the recovered patches and becomes the merged
+ * plane -- no pass-through copy. */
 int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
                      const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
                      const uint8_t* mask_bits, uint8_t* out, void* workspace,

@@ -31,7 +31,7 @@ EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
           "token", "baseline", "decode", "rs")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class NativeError(RuntimeError):
@@ -203,13 +203,14 @@ class NativeModel:
         return out
 
     def recover_u8(self, frames: torch.Tensor, frame_index: torch.Tensor,
-                   mask_bits: torch.Tensor, out: torch.Tensor, b: int, h: int, w: int,
-                   prec: int) -> torch.Tensor:
+                   mask_bits: torch.Tensor, out: torch.Tensor | None, b: int, h: int, w: int,
+                   prec: int) -> torch.Tensor | None:
+        """out=None merges in place into each stream's corrupted-plane slot."""
         ws = self.workspace(b, h, w, prec)
         check(self.lib.nvrec_recover_u8(self.handle, b, h, w, frames.data_ptr(),
                                         frames.shape[0], frame_index.data_ptr(), mask_bits.data_ptr(),
-                                        out.data_ptr(), ws.data_ptr(), ws.numel(), prec,
-                                        stream_ptr()))
+                                        None if out is None else out.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), prec, stream_ptr()))
         return out
 
 

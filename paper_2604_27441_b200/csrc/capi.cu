@@ -200,9 +200,16 @@ int check_arch(const nvrec_config* cfg, int channels) {
 }
 
 // Shared launch sequence after the embedding: blocks, attention, head.
+// In-place merge target (out_u8 == null on the u8 path): stream b's corrupted
+// plane, frames + frame_index[b * F + F - 1] * frame_bytes.
+struct InPlace {
+  uint8_t* frames = nullptr;
+  const int32_t* frame_index = nullptr;
+};
+
 int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bool fast,
                bool pruned, int h, int w, float* out_f32, uint8_t* out_u8,
-               cudaStream_t s) {
+               cudaStream_t s, InPlace ip = {}) {
   const Dims& D = m->D;
   const int b = A.b;
   nvrec::QkvDst dst{};
@@ -251,6 +258,10 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
     ta.dst.rank = (!last && li + 1 == D.layers - 1 && pruned) ? A.rank : nullptr;
     ta.img_h = h; ta.img_w = w; ta.nh = A.nh; ta.nw = A.nw; ta.ns = A.ns;
     ta.out_f32 = out_f32; ta.out_u8 = out_u8;
+    ta.out_frames = ip.frames;
+    ta.out_slot = ip.frame_index ? ip.frame_index + (D.F - 1) : nullptr;
+    ta.slot_stride = D.F;
+    ta.frame_bytes = size_t(h) * w * D.c;
     if (fast && !last && nvrec::token_tc_supported(D) && m->W.tc.blk[li]) {
       const nvrec::BlockW& bw = m->W.blk[li];
       const nvrec::BlockW& bn = m->W.blk[li + 1];
@@ -564,7 +575,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   if (rc) return rc;
   if (m->D.p != 16)
     return fail(NVREC_E_UNSUPPORTED, "u8 recover path needs patch == mask block (16)");
-  if (!frames || !frame_index || !mask_bits || !out)
+  if (!frames || !frame_index || !mask_bits)
     return fail(NVREC_E_INVALID, "null pointer");
   if (n_slots < 1) return fail(NVREC_E_INVALID, "n_slots must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -598,6 +609,14 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   } else {
     rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
     if (rc) return rc;
+  }
+  if (!out) {
+    // in place: the corrupted plane already holds every trusted pixel; only
+    // the masked patches are written (after the embedding read the stack)
+    InPlace ip;
+    ip.frames = const_cast<uint8_t*>(frames);
+    ip.frame_index = frame_index;
+    return run_blocks(m, A, L, fast, true, h, w, nullptr, nullptr, s, ip);
   }
   // the merge base (corrupted plane) is copied only after the embedding has
   // read every stacked frame, so `out` may alias a reference slot (a ring

@@ -167,7 +167,9 @@ __device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, in
       // np.clip(out * 255.0 + 0.5, 0, 255).astype(np.uint8): f32 mul, f32 add
       float q = __fadd_rn(__fmul_rn(sg, 255.f), 0.5f);
       q = fminf(fmaxf(q, 0.f), 255.f);
-      a.out_u8[((size_t(b) * a.img_h + y) * a.img_w + xx) * c + ch] = uint8_t(q);
+      uint8_t* ob = a.out_u8 ? a.out_u8 + size_t(b) * a.img_h * a.img_w * c
+                             : a.out_frames + size_t(a.out_slot[b * a.slot_stride]) * a.frame_bytes;
+      ob[(size_t(y) * a.img_w + xx) * c + ch] = uint8_t(q);
     }
   });
 }

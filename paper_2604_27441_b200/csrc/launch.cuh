@@ -51,6 +51,10 @@ struct TokenArgs {
   int img_h, img_w, nh, nw, ns;
   float* out_f32;       // (b, c, h, w) or null
   uint8_t* out_u8;      // (b, h, w, c) or null
+  uint8_t* out_frames;  // or: merge in place into stream b's corrupted plane,
+  const int32_t* out_slot;  // frames + out_slot[b * slot_stride] * frame_bytes
+  int slot_stride;
+  size_t frame_bytes;
   int P;                // positions per CTA (set by launch_token)
 };
 

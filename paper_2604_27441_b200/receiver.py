@@ -9,9 +9,11 @@ receiver's P-frame finalisation (rgbdstream/receiver.py:211-274):
                      plane (``self.refs[modality]``, receiver.py:244-247) and
                      the corruption mask (codec.py:260-321) -> nvrec_decode
   backend(req)       recovery with the k-frame ring (receiver.py:260-264)
-                     -> nvrec_recover_u8, output straight into the ring
-  ring push          the recovered plane replaces the oldest reference
-                     (receiver.py:268-269), in place
+                     -> nvrec_recover_u8 in place: the masked patches are
+                     written into the decoded plane's own slot
+  ring push          that slot becomes the newest reference and the oldest
+                     leaves the ring (receiver.py:268-269) -- a cyclic slot
+                     schedule, no copies
 
 Per frame time only the compressed bytes travel host -> device (codec header
 + assembled body, ~60-200 KB at 720p instead of a 2.8 MB plane), and the
@@ -23,12 +25,11 @@ fallback policy decides what to display.
 
 from __future__ import annotations
 
-import numpy as np
 import torch
 
 from . import _native
 from .codec import DecodeBatch, DecodeItem, raise_status
-from .recovery import RecoveryEngine, stack_slots
+from .recovery import RecoveryEngine, cyclic_slot_tables
 
 
 class ReceiverPipeline:
@@ -49,30 +50,24 @@ class ReceiverPipeline:
         self.nbuf = nbuf
         dev = init_refs.device
         self.device = dev
-        self.frames = torch.empty((self.k + nbuf, n, h, w, self.c), dtype=torch.uint8, device=dev)
+        # S = k + nbuf slots used cyclically (see RecoveryPipeline): step t
+        # decodes into slot t+k against the newest reference t+k-1
+        self.S = self.k + nbuf
+        self.frames = torch.empty((self.S, n, h, w, self.c), dtype=torch.uint8, device=dev)
         self.frames[:self.k].copy_(init_refs.transpose(0, 1))      # (n, k, ...) -> slot-major
-        self.flat = self.frames.view((self.k + nbuf) * n, h, w, self.c)
-        self.head = 0                                   # ring slot of the oldest reference
+        self.flat = self.frames.view(self.S * n, h, w, self.c)
         nblk = (h // 16) * (w // 16)
         self.dec = [DecodeBatch(n, max_header, max_payload, nblk, max_shards=max_shards,
                                 max_ranges=1, device=dev) for _ in range(nbuf)]
         self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
                          for _ in range(nbuf)]
-        slots = stack_slots(self.k, self.k, self.F)
-        tab = np.empty((self.k, nbuf, n, self.F), np.int32)
-        for hd in range(self.k):
-            for i in range(nbuf):
-                ring = [((hd + j) % self.k) for j in range(self.k)] + [self.k + i]
-                for s in range(n):
-                    tab[hd, i, s] = [ring[x] * n + s for x in slots]
-        self.tables = torch.from_numpy(tab).to(dev)
+        self.tables = cyclic_slot_tables(self.k, nbuf, n, self.F, dev)
         self.s_h2d = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
         self.ev_h2d = [torch.cuda.Event() for _ in range(nbuf)]
         self.ev_cmp = [torch.cuda.Event() for _ in range(nbuf)]
         self.ev_d2h = [torch.cuda.Event() for _ in range(nbuf)]
-        self.ev_slot = [None] * self.k
         self.step = 0
         self.bytes_in = [0] * nbuf
 
@@ -89,11 +84,12 @@ class ReceiverPipeline:
         if self.step >= self.nbuf:
             self.ev_h2d[i].synchronize()
             self.ev_d2h[i].synchronize()
-        hd = self.head
-        newest = (hd - 1) % self.k
+        ph = self.step % self.S
+        st = (self.step + self.k) % self.S              # decoded plane's slot
+        newest = (st - 1) % self.S
         items = []
         for s, (header, body, received, shard_len) in enumerate(frames):
-            items.append(DecodeItem(header, body, self.frames[self.k + i, s],
+            items.append(DecodeItem(header, body, self.frames[st, s],
                                     self.frames[newest, s], n_data=len(received),
                                     received=received, shard_len=shard_len,
                                     body_len=len(body)))
@@ -106,19 +102,17 @@ class ReceiverPipeline:
             # descriptors, headers, flags and the packed bodies: one copy
             dec.dev_in[:dec.used].copy_(dec.host[:dec.used], non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
+        # decode into slot st (last read by step - nbuf's compute, earlier on
+        # s_cmp), then recover in place: st becomes the newest reference
         self.s_cmp.wait_event(self.ev_h2d[i])
-        if self.ev_slot[hd] is not None:
-            self.s_cmp.wait_event(self.ev_slot[hd])
         with torch.cuda.stream(self.s_cmp):
             dec.launch(self.s_cmp, copy=False)
-            self.engine.recover_device(self.flat, self.tables[hd, i], dec.wire, self.frames[hd])
+            self.engine.recover_device(self.flat, self.tables[ph], dec.wire, in_place=True)
             self.ev_cmp[i].record(self.s_cmp)
         self.s_d2h.wait_event(self.ev_cmp[i])
         with torch.cuda.stream(self.s_d2h):
-            self.host_out[i].copy_(self.frames[hd], non_blocking=True)
+            self.host_out[i].copy_(self.frames[st], non_blocking=True)
             self.ev_d2h[i].record(self.s_d2h)
-        self.ev_slot[hd] = self.ev_d2h[i]
-        self.head = (hd + 1) % self.k
         self.step += 1
         return i
 

@@ -51,18 +51,22 @@ class RecoveryEngine:
         return self.model.channels
 
     def recover_device(self, frames: torch.Tensor, frame_index: torch.Tensor,
-                       mask_bits: torch.Tensor, out: torch.Tensor | None = None
-                       ) -> torch.Tensor:
+                       mask_bits: torch.Tensor, out: torch.Tensor | None = None,
+                       in_place: bool = False) -> torch.Tensor | None:
         """All-device batched call.
 
         frames: u8 (n_slots, h, w, c) on the device; frame_index: int32
         (b, stack_len) slot table; mask_bits: u8 (b, ceil(gh*gw/8)).
-        Returns u8 (b, h, w, c) merged planes."""
+        Returns u8 (b, h, w, c) merged planes; with ``in_place`` each stream's
+        corrupted plane (its last slot) becomes the merged plane and nothing
+        is returned (no pass-through copy of the trusted pixels)."""
         nat = self.model.native(frames.device)
         _, h, w, c = frames.shape
         b = frame_index.shape[0]
         if c != self.channels:
             raise ValueError("expected %d channels, got %d" % (self.channels, c))
+        if in_place:
+            return nat.recover_u8(frames, frame_index, mask_bits, None, b, h, w, self.precision)
         if out is None:
             out = torch.empty((b, h, w, c), dtype=torch.uint8, device=frames.device)
         return nat.recover_u8(frames, frame_index, mask_bits, out, b, h, w, self.precision)
@@ -87,6 +91,21 @@ class RecoveryEngine:
         return res if plane.ndim == 3 else res[:, :, 0]
 
 
+def cyclic_slot_tables(k: int, nbuf: int, n: int, F: int, device) -> torch.Tensor:
+    """Slot tables of the cyclic slot-major ring (S = k + nbuf slots of n
+    streams): phase p = step % S reads references p .. p+k-1 (mod S, oldest
+    first, front-padded as ``stack_slots`` does) and the corrupted plane in
+    slot p+k.  Returns int32 (S, n, F) flat indices slot * n + stream."""
+    S = k + nbuf
+    slots = stack_slots(k, k, F)
+    tab = np.empty((S, n, F), np.int32)
+    for p in range(S):
+        ring = [(p + j) % S for j in range(k)] + [(p + k) % S]
+        for s in range(n):
+            tab[p, s] = [ring[x] * n + s for x in slots]
+    return torch.from_numpy(tab).to(device)
+
+
 def grid_shape(h: int, w: int) -> tuple[int, int]:
     return h // MASK_BLOCK, w // MASK_BLOCK
 
@@ -99,16 +118,19 @@ class RecoveryPipeline:
     state.  ``submit`` stages them (pinned host memory), then enqueues
 
       copy stream     H2D of the planes + loss-mask jobs into buffer i
-      compute stream  one CUDA graph: nvrec_loss_mask -> nvrec_recover_u8,
-                      the output written straight into the stream's oldest
-                      reference slot (it becomes the newest reference,
-                      reference receiver.py:268-269 -- no ring copies)
+      compute stream  nvrec_loss_mask -> nvrec_recover_u8 in place: the
+                      recovered patches are written into the corrupted plane's
+                      own slot, which then becomes the newest reference
+                      (reference receiver.py:268-269) -- no pass-through copy,
+                      no ring copies
       copy stream     D2H of the recovered planes
 
     with buffer i = step % nbuf, so the transfers of neighbouring steps
-    overlap the compute.  Device memory is slot-major, ``frames[slot][stream]``:
-    slots 0..k-1 are the reference ring (all streams advance together, so one
-    ring head serves every stream), slots k..k+nbuf-1 the corrupted planes.
+    overlap the compute.  Device memory is slot-major, ``frames[slot][stream]``
+    with S = k + nbuf slots used cyclically (all streams advance together):
+    step t reads the reference ring t .. t+k-1 (mod S, oldest first) and
+    stages its corrupted plane in slot t+k, which joins the ring; slot t
+    leaves it and is next written at step t+nbuf, after step t's compute.
     ``result(handle)`` waits for that step's D2H and returns the pinned host
     array (n, h, w, c); it stays valid for ``nbuf`` more submits."""
 
@@ -124,10 +146,10 @@ class RecoveryPipeline:
         self.nbuf = nbuf
         dev = init_refs.device
         self.device = dev
-        self.frames = torch.empty((self.k + nbuf, n, h, w, self.c), dtype=torch.uint8, device=dev)
+        self.S = self.k + nbuf
+        self.frames = torch.empty((self.S, n, h, w, self.c), dtype=torch.uint8, device=dev)
         self.frames[:self.k].copy_(init_refs.transpose(0, 1))      # (n, k, ...) -> slot-major
-        self.flat = self.frames.view((self.k + nbuf) * n, h, w, self.c)
-        self.head = 0                                  # ring slot of the oldest reference
+        self.flat = self.frames.view(self.S * n, h, w, self.c)
         self.nblk = (h // 16) * (w // 16)
         self.lm = [LossMaskBatch(n, max_header, max_shards, self.nblk, 1, dev)
                    for _ in range(nbuf)]
@@ -135,16 +157,7 @@ class RecoveryPipeline:
                         for _ in range(nbuf)]
         self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
                          for _ in range(nbuf)]
-        # slot tables for every (ring head, buffer): oldest reference first
-        # (front-padded as stack_slots does), the corrupted plane last
-        slots = stack_slots(self.k, self.k, self.F)
-        tab = np.empty((self.k, nbuf, n, self.F), np.int32)
-        for hd in range(self.k):
-            for i in range(nbuf):
-                ring = [((hd + j) % self.k) for j in range(self.k)] + [self.k + i]
-                for sidx in range(n):
-                    tab[hd, i, sidx] = [ring[x] * n + sidx for x in slots]
-        self.tables = torch.from_numpy(tab).to(dev)
+        self.tables = cyclic_slot_tables(self.k, nbuf, n, self.F, dev)
         self.s_h2d = torch.cuda.Stream(dev)
         # one DMA stream reaches ~40 GB/s host->device; four in parallel ~51
         self.s_parts = [torch.cuda.Stream(dev) for _ in range(max(1, min(h2d_streams, n)))]
@@ -153,7 +166,6 @@ class RecoveryPipeline:
         self.ev_h2d = [torch.cuda.Event() for _ in range(nbuf)]
         self.ev_cmp = [torch.cuda.Event() for _ in range(nbuf)]
         self.ev_d2h = [torch.cuda.Event() for _ in range(nbuf)]
-        self.ev_slot = [None] * self.k                 # D2H that last read ring slot r
         self.step = 0
         self.shard_len = shard_len
         self.use_graphs = graphs
@@ -165,28 +177,28 @@ class RecoveryPipeline:
     def d2h_bytes(self) -> int:
         return int(self.host_out[0].numel())
 
-    def _compute(self, hd: int, i: int, stream) -> None:
+    def _compute(self, ph: int, i: int, stream) -> None:
         lib = self.lm[i].lib
         with torch.cuda.stream(stream):
             _native.check(lib.nvrec_loss_mask(ctypes.c_void_p(self.lm[i].dev_in.data_ptr()),
                                               self.lm[i].n,
                                               ctypes.c_void_p(int(stream.cuda_stream))))
-            self.engine.recover_device(self.flat, self.tables[hd, i], self.lm[i].wire,
-                                       self.frames[hd])
+            self.engine.recover_device(self.flat, self.tables[ph], self.lm[i].wire,
+                                       in_place=True)
 
-    def _run(self, hd: int, i: int) -> None:
+    def _run(self, ph: int, i: int) -> None:
         if not self.use_graphs:
-            self._compute(hd, i, self.s_cmp)
+            self._compute(ph, i, self.s_cmp)
             return
-        g = self._graphs.get((hd, i))
+        g = self._graphs.get((ph, i))
         if g is None:
             # warm the launch paths (attributes, workspace) outside capture
             with torch.cuda.stream(self.s_cmp):
-                self._compute(hd, i, self.s_cmp)
+                self._compute(ph, i, self.s_cmp)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.s_cmp):
-                self._compute(hd, i, self.s_cmp)
-            self._graphs[(hd, i)] = g
+                self._compute(ph, i, self.s_cmp)
+            self._graphs[(ph, i)] = g
             # the warm-up consumed this step's inputs and wrote the output
             # slot once; replaying recomputes the same values, so replay only
             # where the warm-up result is not already final
@@ -204,10 +216,11 @@ class RecoveryPipeline:
         if planes is not None:
             self.host_in[i].numpy()[...] = planes
         self.lm[i].stage(frames)
-        hd = self.head
+        ph = self.step % self.S
+        st = (self.step + self.k) % self.S             # this step's corrupted-plane slot
         # H2D: planes into the corrupted-plane slot, loss-mask jobs
         if self.step >= self.nbuf:
-            self.s_h2d.wait_event(self.ev_cmp[i])  # step - nbuf finished reading slot k+i
+            self.s_h2d.wait_event(self.ev_cmp[i])  # step - nbuf read slot st (its oldest ref)
         start = self.s_h2d.record_event()
         per = -(-self.n // len(self.s_parts))
         for p, sp in enumerate(self.s_parts):
@@ -216,24 +229,20 @@ class RecoveryPipeline:
                 continue
             sp.wait_event(start)
             with torch.cuda.stream(sp):
-                self.frames[self.k + i, lo:hi].copy_(self.host_in[i][lo:hi], non_blocking=True)
+                self.frames[st, lo:hi].copy_(self.host_in[i][lo:hi], non_blocking=True)
             self.s_h2d.wait_stream(sp)
         with torch.cuda.stream(self.s_h2d):
             self.lm[i].dev_in.copy_(self.lm[i].host, non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
-        # compute: output goes into the oldest ring slot once its last D2H is done
+        # compute: the recovered patches land in slot st itself
         self.s_cmp.wait_event(self.ev_h2d[i])
-        if self.ev_slot[hd] is not None:
-            self.s_cmp.wait_event(self.ev_slot[hd])
-        self._run(hd, i)
+        self._run(ph, i)
         self.ev_cmp[i].record(self.s_cmp)
         # D2H of the recovered planes (now the newest references)
         self.s_d2h.wait_event(self.ev_cmp[i])
         with torch.cuda.stream(self.s_d2h):
-            self.host_out[i].copy_(self.frames[hd], non_blocking=True)
+            self.host_out[i].copy_(self.frames[st], non_blocking=True)
             self.ev_d2h[i].record(self.s_d2h)
-        self.ev_slot[hd] = self.ev_d2h[i]
-        self.head = (hd + 1) % self.k
         self.step += 1
         return i
 

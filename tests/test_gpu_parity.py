@@ -126,6 +126,29 @@ def test_batched_streams_equal_single():
         assert np.array_equal(out[s], singles[s])
 
 
+@pytest.mark.parametrize("c", [3, 1])
+def test_in_place_merge_equals_out_of_place(c):
+    """out=NULL merges into each stream's corrupted-plane slot: that slot ends
+    up equal to the out-of-place result and every other slot is untouched."""
+    from paper_2604_27441_b200.recovery import RecoveryEngine, pack_grid, stack_slots
+    arch = nvrec_forward.Arch()
+    rng = np.random.default_rng(31 + c)
+    eng = RecoveryEngine(_model(arch, c, make_state(arch, c, 310 + c), "fast"), "fast")
+    B, h, w = 3, 96, 160
+    frames = torch.from_numpy(np.concatenate([textured_u8(rng, 6, h, w, c) for _ in range(B)])).cuda()
+    idx = torch.tensor([[6 * s + i for i in stack_slots(5, 5, 6)] for s in range(B)],
+                       dtype=torch.int32).cuda()
+    bits = torch.from_numpy(np.stack([pack_grid(block_grid(rng, h // 16, w // 16, 0.25))
+                                      for _ in range(B)])).cuda()
+    want = eng.recover_device(frames, idx, bits).cpu().numpy()
+    inplace = frames.clone()
+    assert eng.recover_device(inplace, idx, bits, in_place=True) is None
+    got = inplace.cpu().numpy()
+    for s in range(B):
+        assert np.array_equal(got[6 * s + 5], want[s])
+        assert np.array_equal(got[6 * s:6 * s + 5], frames[6 * s:6 * s + 5].cpu().numpy())
+
+
 # -- reference model-contract tests (pkg/nvrec/tests/test_nvrec_model.py) ------
 
 @pytest.mark.parametrize("k", [1, 3, 5, 7])
