@@ -230,7 +230,8 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
       int nk = 1;
       // the SIMT token kernel (last block) merges key-split partials itself
       const bool defer = last || !nvrec::token_tc_supported(D) || !m->W.tc.blk[li];
-      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits);
+      e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits,
+                                !defer);   // token_tc reads ao as fp16
       ps.kernels(nk);
     } else {
       nvrec::AttnArgs aa{};
@@ -267,7 +268,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
       const nvrec::BlockW& bn = m->W.blk[li + 1];
       nvrec::TokenTcArgs tt{};
       tt.b = b; tt.ns = A.ns; tt.ns_pad = A.ns_pad; tt.nt = D.nt;
-      tt.x = A.x; tt.ao = A.ao;
+      tt.x = A.x; tt.ao = reinterpret_cast<const __half*>(A.ao);
       tt.w_blk = m->W.tc.blk[li];
       tt.w_qkv_next = m->W.tc.blk[li + 1] + 53248;
       tt.b_proj_s = bw.proj_s_b; tt.ln_t_w = bw.ln_t_w; tt.ln_t_b = bw.ln_t_b;

@@ -83,6 +83,7 @@ struct __align__(1024) Smem {
 
 struct TcArgs {
   float* ao;          // [b][nt][ns][64]
+  int ao_half;        // write ao as fp16 (same layout, the token_tc A operand format)
   const int* count;   // compact query count per stream, or null (= ns)
   float* part;        // KV-split partials [split][seq][ns][kPart] or null
   int nt, heads, ns, d, seqs;
@@ -93,6 +94,11 @@ struct TcArgs {
   float scale_log2;
 };
 constexpr int kPart = 36;                              // 32 output dims, m, l, 2 pad (16 B rows)
+
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 
 __device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 * t + (j & 1)) * kTileK); }
 
@@ -454,11 +460,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         } else if (q < nq) {
           const int it = (seq / a.heads) % a.nt, hh = seq % a.heads;
           const float inv = 1.f / l;
-          float4* dst = reinterpret_cast<float4*>(
-              a.ao + (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd);
+          const size_t off = (size_t(b * a.nt + it) * a.ns + q) * a.d + hh * kHd;
+          if (a.ao_half) {
+            // fp16, rounded exactly as token_tc would round the fp32 value
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(a.ao) + off);
 #pragma unroll
-          for (int e = 0; e < kHd; e += 4)
-            dst[e / 4] = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+            for (int e = 0; e < kHd; e += 8)
+              dst[e / 8] = make_uint4(pack_h2(o[e] * inv, o[e + 1] * inv),
+                                      pack_h2(o[e + 2] * inv, o[e + 3] * inv),
+                                      pack_h2(o[e + 4] * inv, o[e + 5] * inv),
+                                      pack_h2(o[e + 6] * inv, o[e + 7] * inv));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(a.ao + off);
+#pragma unroll
+            for (int e = 0; e < kHd; e += 4)
+              dst[e / 4] = make_float4(o[e] * inv, o[e + 1] * inv, o[e + 2] * inv, o[e + 3] * inv);
+          }
         }
       }
     }
@@ -490,7 +507,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
 __global__ void __launch_bounds__(256)
 attn_combine_kernel(const float* __restrict__ part, float* __restrict__ ao,
                     const int* __restrict__ count, int seqs, int splits, int nt, int heads,
-                    int ns, int d) {
+                    int ns, int d, int ao_half) {
   pdl_entry();
   const int seq = blockIdx.y;
   const int b = seq / (nt * heads);
@@ -508,7 +525,9 @@ attn_combine_kernel(const float* __restrict__ part, float* __restrict__ ao,
       L = fmaf(__ldg(p + 33), w, L);
       o = fmaf(__ldg(p + e), w, o);
     }
-    ao[(size_t(b * nt + it) * ns + q) * d + hh * kHd + e] = o / L;
+    const size_t off = (size_t(b * nt + it) * ns + q) * d + hh * kHd + e;
+    if (ao_half) reinterpret_cast<__half*>(ao)[off] = __float2half_rn(o / L);
+    else ao[off] = o / L;
   }
 }
 
@@ -545,7 +564,7 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
-                           int* n_kernels, bool defer_combine, int* splits_out) {
+                           int* n_kernels, bool defer_combine, int* splits_out, bool ao_half) {
   const int seqs = A.b * D.nt * D.heads;
   CUtensorMap tq, tk, tv;
   const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
@@ -560,6 +579,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
     return cudaErrorInvalidValue;
   TcArgs ta;
   ta.ao = A.ao;
+  ta.ao_half = ao_half;
   ta.count = count;
   ta.part = A.part;
   ta.nt = D.nt;
@@ -636,7 +656,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   if (combine) {
     dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
     launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt,
-               D.heads, A.ns, D.d);
+               D.heads, A.ns, D.d, int(ao_half));
   }
   return cudaGetLastError();
 }

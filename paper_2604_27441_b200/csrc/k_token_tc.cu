@@ -167,17 +167,19 @@ token_tc_kernel(TokenTcArgs a) {
     float x[64], y[64];
     // ---- 1. x += proj_s(ao) ------------------------------------------------
     {
-      const float4* ao = reinterpret_cast<const float4*>(a.ao + xrow);
+      // ao arrives in fp16 (attn_tc rounds it exactly as put_row64 would):
+      // its 8 16-byte chunks go straight into the A operand rows
+      const uint4* ao = reinterpret_cast<const uint4*>(a.ao + xrow);
       const float4* xi = reinterpret_cast<const float4*>(a.x + xrow);
 #pragma unroll
+      for (int ki = 0; ki < 8; ++ki)
+        *reinterpret_cast<uint4*>(A + ki * 2048 + m * 16) = valid ? ao[ki] : make_uint4(0, 0, 0, 0);
+#pragma unroll
       for (int q = 0; q < 16; ++q) {
-        float4 v = valid ? ao[q] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 u = valid ? xi[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-        y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
         x[4 * q] = u.x; x[4 * q + 1] = u.y; x[4 * q + 2] = u.z; x[4 * q + 3] = u.w;
       }
     }
-    put_row64(A, m, y);
     gemm_a(0, kOffProjS, 64);
     add64(x, 0, P_ + kPBProjS);
     // ---- 2. qkv_t(LN_t(x)); temporal attention by warp shuffles --------------

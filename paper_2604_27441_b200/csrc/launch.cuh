@@ -88,7 +88,7 @@ cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 bool token_tc_supported(const Dims& D);
 struct TokenTcArgs {
   int b, ns, ns_pad, nt;
-  float* x; const float* ao;
+  float* x; const __half* ao;   // ao in fp16 (written so by attn_tc for this consumer)
   const __half* w_blk;          // this block's fp16 pack (proj_s..fc2)
   const __half* w_qkv_next;     // next block's qkv_s pack
   const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
@@ -108,7 +108,7 @@ cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_
 // *splits_out receives the split count (1 = ao written directly)
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
                            int* n_kernels = nullptr, bool defer_combine = false,
-                           int* splits_out = nullptr);
+                           int* splits_out = nullptr, bool ao_half = false);
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
