@@ -266,7 +266,10 @@ token_tc_kernel(TokenTcArgs a) {
                idesc, kk != 0);
     });
     add64(x, 128, P_ + kPBFc2);
-    if (valid) {
+    int qrow = s;
+    if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
+    // a pruned next block reads the residual rows of masked positions only
+    if (valid && qrow >= 0) {
       float4* xo = reinterpret_cast<float4*>(a.x + xrow);
 #pragma unroll
       for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
@@ -275,8 +278,6 @@ token_tc_kernel(TokenTcArgs a) {
     layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
     put_row64(A, m, y);
     gemm_a(0, kOffQkvS, 192);
-    int qrow = s;
-    if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
     // V^T stores in 4-byte pairs: lanes of adjacent positions (same slice)
     // swap one value per dimension pair, so position pair (2i, 2i+1) of dims
     // (e, e+1) goes out as two 32-bit stores instead of four 16-bit ones
