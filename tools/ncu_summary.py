@@ -6,8 +6,11 @@ import sys
 from collections import Counter
 
 
+FILTER = []
+
+
 def page(rep, name, extra=()):
-    out = subprocess.run(["ncu", "-i", rep, "--page", name, "--csv", *extra],
+    out = subprocess.run(["ncu", "-i", rep, *FILTER, "--page", name, "--csv", *extra],
                          capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
@@ -59,4 +62,7 @@ def main(rep, top=30):
 
 
 if __name__ == "__main__":
+    # ncu_summary.py REPORT [TOP] [LAUNCH_INDEX]: one kernel of a multi-kernel report
+    if len(sys.argv) > 3:
+        FILTER = ["--launch-skip", sys.argv[3], "--launch-count", "1"]
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
