@@ -584,8 +584,11 @@ def main():
         "p50_latency_device_ms": statistics.median(lat_dev),
         "p50_latency_protocol_ms": statistics.median(lat_proto),
         "latency_note": "single stream, one RGB-D frame (both modalities on two CUDA "
-                        "streams), e2e through pinned host buffers incl. H2D of 6 planes "
-                        "per modality and D2H of the result",
+                        "streams), e2e through pinned host buffers incl. H2D of the "
+                        "corrupted plane + loss-mask job per modality (references device-"
+                        "resident) and D2H of the result; _device = inputs resident; "
+                        "_protocol = all 6 planes per modality shipped as the reference "
+                        "wire protocol does",
         "stage_ms_per_step": {k: v / args.steps for k, v in prof.ms.items() if v},
         "stage_note": "per-stage device ms from CUDA-event brackets, both modalities "
                       "serialised on one stream (separate pass)",
