@@ -349,7 +349,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           const float2 nm2 = make_float2(-mn, -mn);
   #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
-            if (rows_live) {
+            if (rows_live && h2 == 1 && valid <= 64) {
+              // the key range's last tile ends inside its first half: P = 0
+              // for the second half without exponentiating masked scores
+              uint32_t z[16];
+  #pragma unroll
+              for (int c = 0; c < 16; ++c) z[c] = 0u;
+              tmem_st16(t_s + 32, z);
+              tmem_st16(t_s + 48, z);
+            } else if (rows_live) {
             uint32_t r[64], pk[32];
             tmem_ld32(t_s + 64 * h2, r);
             tmem_ld32(t_s + 64 * h2 + 32, r + 32);
