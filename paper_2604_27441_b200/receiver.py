@@ -41,7 +41,8 @@ class ReceiverPipeline:
     (n, h, w, c) in pinned host memory and the per-stream decode status."""
 
     def __init__(self, engine: RecoveryEngine, n: int, h: int, w: int, init_refs: torch.Tensor,
-                 max_header: int, max_payload: int, max_shards: int, nbuf: int = 3):
+                 max_header: int, max_payload: int, max_shards: int, nbuf: int = 3,
+                 graphs: bool = True):
         self.engine = engine
         self.n, self.h, self.w = n, h, w
         self.c = engine.channels
@@ -62,6 +63,12 @@ class ReceiverPipeline:
         self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
                          for _ in range(nbuf)]
         self.tables = cyclic_slot_tables(self.k, nbuf, n, self.F, dev)
+        # the step's slot table rides in with its inputs, so one CUDA graph
+        # (decode + recovery) per buffer set serves every ring phase
+        self.tab_cur = torch.empty((nbuf, n, self.F), dtype=torch.int32, device=dev)
+        self.nat = engine.model.native(dev)          # weights snapshotted
+        self.use_graphs = graphs
+        self._graphs = {}
         self.s_h2d = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
@@ -101,20 +108,43 @@ class ReceiverPipeline:
         with torch.cuda.stream(self.s_h2d):
             # descriptors, headers, flags and the packed bodies: one copy
             dec.dev_in[:dec.used].copy_(dec.host[:dec.used], non_blocking=True)
+            self.tab_cur[i].copy_(self.tables[ph], non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
         # decode into slot st (last read by step - nbuf's compute, earlier on
         # s_cmp), then recover in place: st becomes the newest reference
         self.s_cmp.wait_event(self.ev_h2d[i])
-        with torch.cuda.stream(self.s_cmp):
-            dec.launch(self.s_cmp, copy=False)
-            self.engine.recover_device(self.flat, self.tables[ph], dec.wire, in_place=True)
-            self.ev_cmp[i].record(self.s_cmp)
+        self._run(i)
+        self.ev_cmp[i].record(self.s_cmp)
         self.s_d2h.wait_event(self.ev_cmp[i])
         with torch.cuda.stream(self.s_d2h):
             self.host_out[i].copy_(self.frames[st], non_blocking=True)
             self.ev_d2h[i].record(self.s_d2h)
         self.step += 1
         return i
+
+    def _compute(self, i: int) -> None:
+        dec = self.dec[i]
+        with torch.cuda.stream(self.s_cmp):
+            dec.launch(self.s_cmp, copy=False)
+            self.engine.recover_device(self.flat, self.tab_cur[i], dec.wire, in_place=True,
+                                       native=self.nat)
+
+    def _run(self, i: int) -> None:
+        if not self.use_graphs:
+            self._compute(i)
+            return
+        g = self._graphs.get(i)
+        if g is None:
+            # first use: run eagerly (warms attributes and the workspace), then
+            # capture for the following steps of this buffer set
+            self._compute(i)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.s_cmp):
+                self._compute(i)
+            self._graphs[i] = g
+            return
+        with torch.cuda.stream(self.s_cmp):
+            g.replay()
 
     def result(self, handle: int, check: bool = True):
         """(planes (n, h, w, c), per-stream decode status codes).  With

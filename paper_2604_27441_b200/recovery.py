@@ -52,7 +52,7 @@ class RecoveryEngine:
 
     def recover_device(self, frames: torch.Tensor, frame_index: torch.Tensor,
                        mask_bits: torch.Tensor, out: torch.Tensor | None = None,
-                       in_place: bool = False) -> torch.Tensor | None:
+                       in_place: bool = False, native=None) -> torch.Tensor | None:
         """All-device batched call.
 
         frames: u8 (n_slots, h, w, c) on the device; frame_index: int32
@@ -60,7 +60,9 @@ class RecoveryEngine:
         Returns u8 (b, h, w, c) merged planes; with ``in_place`` each stream's
         corrupted plane (its last slot) becomes the merged plane and nothing
         is returned (no pass-through copy of the trusted pixels)."""
-        nat = self.model.native(frames.device)
+        # native: a handle the caller resolved once (serving loops), which
+        # skips the per-call weight-change check
+        nat = native if native is not None else self.model.native(frames.device)
         _, h, w, c = frames.shape
         b = frame_index.shape[0]
         if c != self.channels:
@@ -136,7 +138,7 @@ class RecoveryPipeline:
 
     def __init__(self, engine: RecoveryEngine, n: int, h: int, w: int,
                  shard_len: int, max_header: int, max_shards: int, init_refs: torch.Tensor,
-                 nbuf: int = 3, graphs: bool = False, h2d_streams: int = 4):
+                 nbuf: int = 3, graphs: bool = True, h2d_streams: int = 4):
         from .lossmask import LossMaskBatch
         self.engine = engine
         self.n, self.h, self.w = n, h, w
@@ -158,6 +160,12 @@ class RecoveryPipeline:
         self.host_out = [torch.empty((n, h, w, self.c), dtype=torch.uint8).pin_memory()
                          for _ in range(nbuf)]
         self.tables = cyclic_slot_tables(self.k, nbuf, n, self.F, dev)
+        # per buffer set: the step's slot table, copied in with its inputs, so
+        # one CUDA graph per buffer set serves every ring phase
+        self.tab_cur = torch.empty((nbuf, n, self.F), dtype=torch.int32, device=dev)
+        # the weights are snapshotted for the pipeline's lifetime (re-create
+        # it after loading new weights)
+        self.nat = engine.model.native(dev)
         self.s_h2d = torch.cuda.Stream(dev)
         # one DMA stream reaches ~40 GB/s host->device; four in parallel ~51
         self.s_parts = [torch.cuda.Stream(dev) for _ in range(max(1, min(h2d_streams, n)))]
@@ -177,28 +185,28 @@ class RecoveryPipeline:
     def d2h_bytes(self) -> int:
         return int(self.host_out[0].numel())
 
-    def _compute(self, ph: int, i: int, stream) -> None:
+    def _compute(self, i: int, stream) -> None:
         lib = self.lm[i].lib
         with torch.cuda.stream(stream):
             _native.check(lib.nvrec_loss_mask(ctypes.c_void_p(self.lm[i].dev_in.data_ptr()),
                                               self.lm[i].n,
                                               ctypes.c_void_p(int(stream.cuda_stream))))
-            self.engine.recover_device(self.flat, self.tables[ph], self.lm[i].wire,
-                                       in_place=True)
+            self.engine.recover_device(self.flat, self.tab_cur[i], self.lm[i].wire,
+                                       in_place=True, native=self.nat)
 
-    def _run(self, ph: int, i: int) -> None:
+    def _run(self, i: int) -> None:
         if not self.use_graphs:
-            self._compute(ph, i, self.s_cmp)
+            self._compute(i, self.s_cmp)
             return
-        g = self._graphs.get((ph, i))
+        g = self._graphs.get(i)
         if g is None:
             # warm the launch paths (attributes, workspace) outside capture
             with torch.cuda.stream(self.s_cmp):
-                self._compute(ph, i, self.s_cmp)
+                self._compute(i, self.s_cmp)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.s_cmp):
-                self._compute(ph, i, self.s_cmp)
-            self._graphs[(ph, i)] = g
+                self._compute(i, self.s_cmp)
+            self._graphs[i] = g
             # the warm-up consumed this step's inputs and wrote the output
             # slot once; replaying recomputes the same values, so replay only
             # where the warm-up result is not already final
@@ -233,10 +241,11 @@ class RecoveryPipeline:
             self.s_h2d.wait_stream(sp)
         with torch.cuda.stream(self.s_h2d):
             self.lm[i].dev_in.copy_(self.lm[i].host, non_blocking=True)
+            self.tab_cur[i].copy_(self.tables[ph], non_blocking=True)
             self.ev_h2d[i].record(self.s_h2d)
         # compute: the recovered patches land in slot st itself
         self.s_cmp.wait_event(self.ev_h2d[i])
-        self._run(ph, i)
+        self._run(i)
         self.ev_cmp[i].record(self.s_cmp)
         # D2H of the recovered planes (now the newest references)
         self.s_d2h.wait_event(self.ev_cmp[i])
