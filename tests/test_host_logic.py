@@ -75,3 +75,30 @@ def test_pframe_received_flags():
     assert fr.received_flags().tolist() == [1, 0, 1, 0]
     fr = PFrameShards(b"", 3, np.array([True, False, True]), 1024, 10)
     assert fr.received_flags().tolist() == [1, 0, 1]
+
+
+def test_cyclic_slot_ring_schedule():
+    """The serving pipelines' cyclic slot schedule: step t reads references
+    t..t+k-1 (mod S, oldest first) and stages its plane in slot t+k, which is
+    the newest reference of step t+1; a slot is re-staged only nbuf steps
+    after the last step that read it (the pipeline's ev_cmp wait)."""
+    from paper_2604_27441_b200.recovery import cyclic_slot_tables
+    k, nbuf, n, F = 5, 3, 2, 6
+    S = k + nbuf
+    tab = cyclic_slot_tables(k, nbuf, n, F, "cpu").numpy()
+    assert tab.shape == (S, n, F)
+    last_read = {}
+    for t in range(40):
+        p = t % S
+        slots = tab[p] // n
+        assert (tab[p] % n == np.arange(n)[:, None]).all()      # stream s reads its own planes
+        ring, staged = list(slots[0, :-1]), int(slots[0, -1])
+        assert ring == [(t + j) % S for j in range(k)]
+        assert staged == (t + k) % S and staged not in ring
+        if t > 0:
+            prev = tab[(t - 1) % S][0] // n
+            assert ring[-1] == prev[-1]                          # last step's plane is newest
+        if staged in last_read:
+            assert t - last_read[staged] >= nbuf
+        for s in ring:
+            last_read[s] = t
