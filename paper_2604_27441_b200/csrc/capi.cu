@@ -134,7 +134,7 @@ void transpose_into(std::vector<float>& dst, const float* w, int out, int in) {
 }
 
 struct WorkspaceLayout {
-  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, redo, total;
+  size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, redo, xh, total;
 };
 
 WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
@@ -153,6 +153,7 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
   L.ao = take(tok * D.d * 4);
   const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(D);
   if (fast) {
+    L.xh = take(tok * D.d * 2);
     L.qh = take(seqrows * 2);
     L.kh = take(seqrows * 2);
     L.vth = take(seqrows * 2);
@@ -166,7 +167,7 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
     L.q = take(seqrows * 4);
     L.k = take(seqrows * 4);
     L.v = take(seqrows * 4);
-    L.qh = L.kh = L.vth = L.part = L.redo = SIZE_MAX;
+    L.qh = L.kh = L.vth = L.part = L.redo = L.xh = SIZE_MAX;
   }
   L.list = take(size_t(b) * ns * 4);
   L.rank = take(size_t(b) * ns * 4);
@@ -269,6 +270,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bo
       nvrec::TokenTcArgs tt{};
       tt.b = b; tt.ns = A.ns; tt.ns_pad = A.ns_pad; tt.nt = D.nt;
       tt.x = A.x; tt.ao = reinterpret_cast<const __half*>(A.ao);
+      tt.xh = (li == 0 && A.x_half) ? A.xh : nullptr;
       tt.w_blk = m->W.tc.blk[li];
       tt.w_qkv_next = m->W.tc.blk[li + 1] + 53248;
       tt.b_proj_s = bw.proj_s_b; tt.ln_t_w = bw.ln_t_w; tt.ln_t_b = bw.ln_t_b;
@@ -489,6 +491,8 @@ static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout
                            int h, int w) {
   nvrec::Act A{};
   A.x = at<float>(ws, L.x);
+  A.xh = L.xh == SIZE_MAX ? nullptr : at<__half>(ws, L.xh);
+  A.x_half = false;
   A.ao = at<float>(ws, L.ao);
   A.q = at<float>(ws, L.q);
   A.k = at<float>(ws, L.k);
@@ -600,6 +604,10 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     ea.rank = A.rank;
     ea.qrank = m->D.layers == 1 ? A.rank : nullptr;
     ea.x = A.x; ea.qh = A.qh; ea.kh = A.kh; ea.vth = A.vth;
+    // the embedding output goes to block 0's tensor-core tail in fp16 (half
+    // the traffic of that one hand-off; the tail keeps the residual in fp32)
+    A.x_half = A.xh && m->D.layers > 1 && nvrec::token_tc_supported(m->D) && m->W.tc.blk[0];
+    ea.xh = A.x_half ? A.xh : nullptr;
     ea.b = b; ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns; ea.ns_pad = A.ns_pad;
     cudaError_t e2;
     {

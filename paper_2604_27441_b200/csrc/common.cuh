@@ -115,6 +115,8 @@ struct ModelW {
 // Token-stream buffers of one forward (workspace carve-up).
 struct Act {
   float* x;          // [b][nt][ns][d] residual stream
+  __half* xh;        // fast path: fp16 copy of the embedding output for block 0's
+  bool x_half;       //   tensor-core tail (set when the embed wrote xh instead of x)
   float* ao;         // [b][nt][nrow][d] spatial-attention output (compact rows
                      //   when `list` is set: row r <-> list[r])
   float* q;          // f32 path: [b*nt*heads][nq_pad][hd]; rows compact when

@@ -237,7 +237,13 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       if (mterm) v += sm.par[128 + o];
       x[o] = v + sm.par[64 + o];
     }
-    if (valid) {
+    if (valid && a.xh) {
+      uint4* xo = reinterpret_cast<uint4*>(a.xh + (size_t(b * a.D.nt + it) * a.ns + s) * 64);
+#pragma unroll
+      for (int o = 0; o < 64; o += 8)
+        xo[o / 8] = make_uint4(pack_h2(x[o], x[o + 1]), pack_h2(x[o + 2], x[o + 3]),
+                               pack_h2(x[o + 4], x[o + 5]), pack_h2(x[o + 6], x[o + 7]));
+    } else if (valid) {
       float4* xo = reinterpret_cast<float4*>(a.x + (size_t(b * a.D.nt + it) * a.ns + s) * 64);
 #pragma unroll
       for (int o = 0; o < 64; o += 4) xo[o / 4] = make_float4(x[o], x[o + 1], x[o + 2], x[o + 3]);

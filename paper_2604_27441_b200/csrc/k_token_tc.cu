@@ -170,14 +170,30 @@ token_tc_kernel(TokenTcArgs a) {
       // ao arrives in fp16 (attn_tc rounds it exactly as put_row64 would):
       // its 8 16-byte chunks go straight into the A operand rows
       const uint4* ao = reinterpret_cast<const uint4*>(a.ao + xrow);
-      const float4* xi = reinterpret_cast<const float4*>(a.x + xrow);
 #pragma unroll
       for (int ki = 0; ki < 8; ++ki)
         *reinterpret_cast<uint4*>(A + ki * 2048 + m * 16) = valid ? ao[ki] : make_uint4(0, 0, 0, 0);
+      if (a.xh) {
+        // block 0: the embedding handed the residual over in fp16
+        const uint4* xi = reinterpret_cast<const uint4*>(a.xh + xrow);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        float4 u = valid ? xi[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-        x[4 * q] = u.x; x[4 * q + 1] = u.y; x[4 * q + 2] = u.z; x[4 * q + 3] = u.w;
+        for (int q = 0; q < 8; ++q) {
+          const uint4 u = valid ? xi[q] : make_uint4(0, 0, 0, 0);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+            x[8 * q + 2 * e] = f.x;
+            x[8 * q + 2 * e + 1] = f.y;
+          }
+        }
+      } else {
+        const float4* xi = reinterpret_cast<const float4*>(a.x + xrow);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float4 u = valid ? xi[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[4 * q] = u.x; x[4 * q + 1] = u.y; x[4 * q + 2] = u.z; x[4 * q + 3] = u.w;
+        }
       }
     }
     gemm_a(0, kOffProjS, 64);

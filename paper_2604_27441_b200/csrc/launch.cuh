@@ -79,6 +79,7 @@ struct EmbedTcArgs {
   const int* rank;                // masked patches (block mask), required
   const int* qrank;               // compact Q rows (block 0 pruned) or null
   float* x;
+  __half* xh;                     // or: the embedding output in fp16 (token_tc input)
   __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
   int b, h, w, nh, nw, ns, ns_pad;
 };
@@ -89,6 +90,7 @@ bool token_tc_supported(const Dims& D);
 struct TokenTcArgs {
   int b, ns, ns_pad, nt;
   float* x; const __half* ao;   // ao in fp16 (written so by attn_tc for this consumer)
+  const __half* xh;             // residual input in fp16 (from embed_tc) or null = x
   const __half* w_blk;          // this block's fp16 pack (proj_s..fc2)
   const __half* w_qkv_next;     // next block's qkv_s pack
   const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
