@@ -178,7 +178,7 @@ __device__ __forceinline__ void token_tile(const TokenArgs& a, int b, int r0, in
 // over the stream's masked-patch list (the count lives on the device, so the
 // grid is sized for the GPU, not for the worst case).
 template <bool kNarrow>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, kNarrow ? 1 : 2)
 token_kernel(TokenArgs a) {
   pdl_wait();
   extern __shared__ float smem[];

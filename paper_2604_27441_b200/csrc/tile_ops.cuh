@@ -81,8 +81,24 @@ __device__ __forceinline__ void tile_gemm_narrow(const float* in, int ldi, int n
       const float* a0 = in + t * ldi;
       const float* w = Wt + cq * 4;
       float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-#pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
+      // 16 weight rows in flight per batch (the phase is L2-latency bound);
+      // same accumulation order as the plain loop
+      int k = k0;
+      for (; k + 16 <= k1; k += 16) {
+        float4 wv[16];
+        float xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          wv[u] = __ldg(reinterpret_cast<const float4*>(w + size_t(k + u) * N));
+          xv[u] = a0[k + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          c0 = fmaf(xv[u], wv[u].x, c0); c1 = fmaf(xv[u], wv[u].y, c1);
+          c2 = fmaf(xv[u], wv[u].z, c2); c3 = fmaf(xv[u], wv[u].w, c3);
+        }
+      }
+      for (; k < k1; ++k) {
         const float4 wv = __ldg(reinterpret_cast<const float4*>(w + size_t(k) * N));
         const float x0 = a0[k];
         c0 = fmaf(x0, wv.x, c0); c1 = fmaf(x0, wv.y, c1);
