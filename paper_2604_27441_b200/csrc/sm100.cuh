@@ -262,14 +262,22 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 // 2^(v-j) on [-0.5, 0.5] (rel. error 6e-4, below bf16 P's 3.9e-3), then add
 // j to the exponent field.  Since (bits(1.5*2^23) << 23) == 0 mod 2^32, the
 // exponent add is a single IMAD: bits(p) + bits(t) * 2^23.
+__device__ __forceinline__ float sat_ffma(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float2 exp2_poly2(float2 v) {
-  v.x = fminf(fmaxf(v.x, -127.f), 127.f);    // the exponent add must not wrap
-  v.y = fminf(fmaxf(v.y, -127.f), 127.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);
-  const float2 nmagic = make_float2(-12582912.f, -12582912.f);
-  const float2 t = fadd2(v, magic);
-  const float2 j = fadd2(t, nmagic);
-  const float2 f = fadd2(v, make_float2(-j.x, -j.y));
+  // the exponent add must not wrap: clamp v to [-127, 127] with one
+  // saturating FMA per element, u = sat((v + 127) / 254), and carry the affine
+  // map through the rounding (v' = 254 u - 127 differs from v by <= 1.5e-5)
+  const float2 u = make_float2(sat_ffma(v.x, 1.f / 254.f, 127.f / 254.f),
+                               sat_ffma(v.y, 1.f / 254.f, 127.f / 254.f));
+  const float2 k254 = make_float2(254.f, 254.f);
+  const float2 t = ffma2(u, k254, make_float2(12582912.f - 127.f, 12582912.f - 127.f));
+  const float2 c = fadd2(make_float2(12582912.f - 127.f, 12582912.f - 127.f),
+                         make_float2(-t.x, -t.y));            // -127 - j (exact)
+  const float2 f = ffma2(u, k254, c);                            // v' - j in [-0.5, 0.5]
   float2 p = ffma2(make_float2(0.0555041087f, 0.0555041087f), f,
                    make_float2(0.2402265070f, 0.2402265070f));
   p = ffma2(p, f, make_float2(0.6931471806f, 0.6931471806f));
