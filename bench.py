@@ -120,7 +120,7 @@ class ModalityWork:
         from paper_2604_27441_b200 import Checkpoint, ModelConfig
         from paper_2604_27441_b200.lossmask import LossMaskBatch, PFrameShards
         from paper_2604_27441_b200.recovery import RecoveryEngine, stack_slots
-        from paper_2604_27441_b200.synth import GilbertElliott, p_frame_shards
+        from tools.synth import GilbertElliott, p_frame_shards
 
         S = len(stream_ids)
         self.name, self.c, self.S = name, c, S
@@ -219,9 +219,9 @@ class ReceiverWork:
     decoded + recovered on the GPU by ReceiverPipeline."""
 
     def __init__(self, name, c, L, stream_ids, device, engine, n_frames=6):
-        from paper_2604_27441_b200 import synth
+        from tools import synth
         from paper_2604_27441_b200.receiver import ReceiverPipeline
-        from paper_2604_27441_b200.synth import GilbertElliott
+        from tools.synth import GilbertElliott
         self.name, self.c, self.S = name, c, len(stream_ids)
         seqs, init = [], []
         max_hdr = max_body = max_nd = 0

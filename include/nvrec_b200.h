@@ -134,7 +134,9 @@ typedef struct nvrec_lossmask_job {
 } nvrec_lossmask_job;
 
 /* Batched loss-mask kernel: jobs is a DEVICE array of n_jobs descriptors.
- * Bit-exact with the reference receiver+codec. */
+ * Bit-exact with the reference receiver+codec.  A job whose status is
+ * nonzero gets all ceil(grid_capacity/8) wire-bit bytes cleared, so a
+ * recovery launch consuming them leaves that stream's plane untouched. */
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream);
 
 /* Status codes written to nvrec_lossmask_job.status[0] (0 = ok):
@@ -166,7 +168,12 @@ typedef struct nvrec_decode_job {
 } nvrec_decode_job;
 
 /* Batched decode: jobs is a DEVICE array; max_blocks >= every job's block
- * count (h/block * w/block).  Bit-exact with the reference. */
+ * count (h/block * w/block).  Bit-exact with the reference.  Error policy
+ * (LOST_FRAME, receiver.py:244-248): a job that ends with a nonzero status
+ * has its wire bits cleared and, when it has a reference distinct from
+ * plane, plane_capacity bytes of the reference copied into plane (the
+ * reference must span plane_capacity bytes), so the slot repeats the newest
+ * displayable plane instead of holding a stale one. */
 int nvrec_decode(const nvrec_decode_job* jobs, int32_t n_jobs, int32_t max_blocks, void* stream);
 
 /* Reed-Solomon erasure reconstruction (fec.rs_reconstruct, fec.py:144-163).

@@ -27,8 +27,9 @@ Pinning
 -------
 The oracle is pinned against golden vectors produced by running the
 UNMODIFIED reference in the build container (``tests/golden/make_golden.py``
-imports ``/root/reference``); ``tests/test_oracle_golden.py`` checks it.  The
-loss-mask oracle is additionally checked against the reference's own test
-expectations (``pkg/tests/test_codec.py:101-189``) in
-``tests/test_lossmask_oracle.py``.
+imports ``/root/reference``); ``tests/test_oracle_golden.py`` checks the
+model, ``_recover``, loss-mask (216 trials through the reference
+``Receiver._finalize_p`` plus the ``codec.decode`` tail rule) and baseline
+restatements, ``tests/test_codec_oracle.py`` the codec/RS restatement, and
+``tests/test_ssim_oracle.py`` the SSIM metric restatement.
 """

@@ -178,6 +178,9 @@ class DecodeBatch:
             mk.status = self.status[j].data_ptr()
             mk.grid_capacity = self.max_blocks
             job.payload = base + po
+            if it.reference is not None and it.reference.numel() < it.out.numel():
+                # the error policy copies plane_capacity bytes of the reference
+                raise ValueError("frame %d: reference smaller than the output plane" % j)
             job.reference = it.reference.data_ptr() if it.reference is not None else None
             job.plane = it.out.data_ptr()
             job.plane_capacity = it.out.numel()

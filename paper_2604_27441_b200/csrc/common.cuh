@@ -32,6 +32,18 @@ __device__ __forceinline__ void pdl_entry() {
 }
 bool pdl_enabled();   // NVREC_PDL=0 turns the attribute off (A/B, debugging)
 
+// Per-device launch facts (capi.cu).  The dynamic shared-memory opt-in is a
+// property of the device context, so it is recorded per (kernel, device)
+// under a mutex and marked done only after cudaFuncSetAttribute succeeded:
+// a second GPU in the same process, or two host threads racing to the first
+// launch, still launch with the attribute set.
+cudaError_t smem_optin(const void* kernel, int bytes);
+template <typename... P>
+inline cudaError_t smem_optin(void (*kernel)(P...), int bytes) {
+  return smem_optin(reinterpret_cast<const void*>(kernel), bytes);
+}
+int sm_count();       // multiprocessors of the current device
+
 // Only light kernels (small CTAs, a few SMs' worth of resources) take the
 // attribute: a heavy successor launched early parks CTAs on every SM while it
 // waits, which starves the concurrent stream of the other modality (measured:

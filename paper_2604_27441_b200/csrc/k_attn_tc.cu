@@ -596,19 +596,17 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.d = D.d;
   ta.seqs = seqs;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
+  {
     const int s2 = int(sizeof(Smem<2>) + 1024), s1 = int(sizeof(Smem<1>) + 1024);
-    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    cudaFuncSetAttribute(attn_tc_kernel<false, false, false, 2>, attr, s2);
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, false, 2>, attr, s2);
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, true, 2>, attr, s2);
-    cudaFuncSetAttribute(attn_tc_kernel<true, false, false, 1>, attr, s1);
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, false, 1>, attr, s1);
-    cudaFuncSetAttribute(attn_tc_kernel<true, true, true, 1>, attr, s1);
+    cudaError_t e;
+    if ((e = smem_optin(attn_tc_kernel<false, false, false, 2>, s2)) != cudaSuccess ||
+        (e = smem_optin(attn_tc_kernel<true, true, false, 2>, s2)) != cudaSuccess ||
+        (e = smem_optin(attn_tc_kernel<true, true, true, 2>, s2)) != cudaSuccess ||
+        (e = smem_optin(attn_tc_kernel<true, false, false, 1>, s1)) != cudaSuccess ||
+        (e = smem_optin(attn_tc_kernel<true, true, false, 1>, s1)) != cudaSuccess ||
+        (e = smem_optin(attn_tc_kernel<true, true, true, 1>, s1)) != cudaSuccess)
+      return e;
   }
   // Dense launch: two query tiles per CTA, one CTA per SM (all of TMEM).  A
   // pruned launch (compact masked-patch queries, count on the device): one

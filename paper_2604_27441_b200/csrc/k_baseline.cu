@@ -255,7 +255,7 @@ cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t
   const size_t plane_bytes = size_t(h) * w * c;
   e = cudaMemcpyAsync(match_out, planes, plane_bytes * b, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return e;
-  dim3 grid(std::min(ns, 2 * 148), b);
+  dim3 grid(std::min(ns, 2 * sm_count()), b);
   if (c == 3)
     launch_pdl(baseline_match_kernel<3>, grid, 320, 0, s, planes, refs, mask_bits, list, count,
                                                   match_out, h, w, ns, nbytes);

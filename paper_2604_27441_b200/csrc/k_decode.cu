@@ -26,10 +26,12 @@
 //                         encoder produces, because runs break at block
 //                         boundaries (codec.py:105-131).  Otherwise it raises
 //                         the frame's slow flag.
-//   decode_slow_kernel    frames with the slow flag only: one thread replays
+//   decode_final_kernel   frames with the slow flag only: one thread replays
 //                         the literal reference semantics (python slicing of
 //                         each range, concatenation, records straddling
-//                         ranges, the two error checks in reference order).
+//                         ranges, the two error checks in reference order);
+//                         then undecodable frames get the error policy
+//                         (plane = decode reference, wire bits cleared).
 // All four are stream-ordered and graph capturable; nothing syncs the host.
 #include "launch.cuh"
 #include "lossmask.cuh"
@@ -236,10 +238,8 @@ decode_present_kernel(const nvrec_decode_job* __restrict__ jobs) {
 }
 
 // Literal replay of codec.py:283-317 for frames the fast path rejected.
-__global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
-  pdl_entry();
-  const nvrec_decode_job& jr = jobs[blockIdx.x];
-  if (threadIdx.x != 0 || jr.mask.status[0] != 0 || jr.scratch[0] == 0) return;
+__device__ void decode_slow(const nvrec_decode_job& jr) {
+  if (jr.mask.status[0] != 0 || jr.scratch[0] == 0) return;
   const Fixed f = read_fixed(jr.mask.header);
   const uint8_t* offs = jr.mask.header + 14 + f.bitmap_len;
   const int32_t* brank = jr.scratch + 4;
@@ -316,14 +316,42 @@ __global__ void decode_slow_kernel(const nvrec_decode_job* __restrict__ jobs) {
   }
 }
 
+// Last launch per batch: the slow path (thread 0), then the error policy.
+// A frame whose decode failed (UndecodableError -> LOST_FRAME, receiver.py:
+// 244-248) is not displayed by the reference and leaves its references
+// alone; here its slot joins the cyclic ring, so it receives a copy of the
+// decode reference (the newest displayable plane: the next P-frame decodes
+// against the same plane as in the reference) and its wire bits are cleared
+// (the recovery launch that follows in the same graph changes nothing).
+__global__ void __launch_bounds__(256) decode_final_kernel(const nvrec_decode_job* __restrict__ jobs) {
+  pdl_entry();
+  const nvrec_decode_job& jr = jobs[blockIdx.x];
+  if (threadIdx.x == 0) decode_slow(jr);
+  __syncthreads();
+  if (jr.mask.status[0] == 0) return;
+  if (jr.mask.wire_bits)
+    for (int t = threadIdx.x; t < (jr.mask.grid_capacity + 7) / 8; t += blockDim.x)
+      jr.mask.wire_bits[t] = 0;
+  const uint8_t* ref = jr.reference;
+  uint8_t* out = jr.plane;
+  if (!ref || ref == out) return;
+  const size_t bytes = size_t(jr.plane_capacity);
+  if (((reinterpret_cast<uintptr_t>(ref) | reinterpret_cast<uintptr_t>(out) | bytes) & 15) == 0) {
+    for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(out)[i] = __ldg(reinterpret_cast<const uint4*>(ref) + i);
+  } else {
+    for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) out[i] = ref[i];
+  }
+}
+
 cudaError_t launch_decode(const nvrec_decode_job* jobs, int n_jobs, int max_blocks,
                           cudaStream_t s) {
   if (n_jobs <= 0) return cudaSuccess;
   launch_pdl(decode_parse_kernel, n_jobs, kParseThreads, kParseStage, s, jobs);
-  launch_pdl(decode_copy_kernel, dim3((2 * 148 + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s, jobs);
+  launch_pdl(decode_copy_kernel, dim3((2 * sm_count() + n_jobs - 1) / n_jobs * 2, n_jobs), kThreads, 0, s, jobs);
   dim3 grid((max_blocks + 4 * kWarps - 1) / (4 * kWarps), n_jobs);
   launch_pdl(decode_present_kernel, grid, kThreads, 0, s, jobs);
-  launch_pdl(decode_slow_kernel, n_jobs, 32, 0, s, jobs);
+  launch_pdl(decode_final_kernel, n_jobs, 256, 0, s, jobs);
   return cudaGetLastError();
 }
 

@@ -206,10 +206,10 @@ cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s) {
   dim3 grid(ceil_div(a.ns, kEmbTok), a.D.nt, b);
   size_t smem = embed_smem_bytes(a.D);
   if (u8) {
-    cudaFuncSetAttribute(embed_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (cudaError_t e = smem_optin(embed_kernel<true>, int(smem))) return e;
     launch_seq(embed_kernel<true>, grid, kEmbThreads, smem, s, a);
   } else {
-    cudaFuncSetAttribute(embed_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (cudaError_t e = smem_optin(embed_kernel<false>, int(smem))) return e;
     launch_seq(embed_kernel<false>, grid, kEmbThreads, smem, s, a);
   }
   return cudaGetLastError();
@@ -225,7 +225,7 @@ cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s) {
 cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index, int F,
                               size_t frame_bytes, uint8_t* out, int b, cudaStream_t s) {
   int blocks = int((frame_bytes / 16 + 255) / 256);
-  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks > sm_count() * 4) blocks = sm_count() * 4;
   launch_pdl(copy_plane_kernel, dim3(blocks, b), 256, 0, s, frames, frame_index, F, frame_bytes, out);
   return cudaGetLastError();
 }

@@ -340,12 +340,7 @@ cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const size_t smem = sizeof(EmbSmem<C>) + 128;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(embed_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(embed_tc_kernel<C>, int(smem))) return e;
   const int tiles = ((a.nh + kTh - 1) / kTh) * ((a.nw + kTw - 1) / kTw);
   launch_seq(embed_tc_kernel<C>, dim3(tiles, a.D.nt, a.b), kThreads, smem, s, tm, a, *a.tcw);
   return cudaGetLastError();

@@ -244,12 +244,8 @@ cudaError_t launch_rs(const nvrec_rs_job* jobs, int n_jobs, int max_shard_len, i
   const int units = word ? (max_shard_len + 3) / 4 : max_shard_len;
   dim3 grid((units + kThreads - 1) / kThreads, n_jobs);
   const size_t smem = (size_t(max_coef) + 15) & ~size_t(15);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rs_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxCoef + 16);
-    cudaFuncSetAttribute(rs_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxCoef + 16);
-    attr = true;
-  }
+  if (cudaError_t e = smem_optin(rs_kernel<true>, kMaxCoef + 16)) return e;
+  if (cudaError_t e = smem_optin(rs_kernel<false>, kMaxCoef + 16)) return e;
   if (word) launch_pdl(rs_kernel<true>, grid, kThreads, smem, s, jobs);
   else launch_pdl(rs_kernel<false>, grid, kThreads, smem, s, jobs);
   return cudaGetLastError();

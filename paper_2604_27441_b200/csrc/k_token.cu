@@ -206,12 +206,12 @@ cudaError_t launch_token(const TokenArgs& a_in, int b, int max_rows, cudaStream_
   a.P = narrow ? 1 : max(1, 48 / a.D.nt);
   size_t smem = token_smem_bytes(a.D, a.P);
   dim3 grid(ceil_div(max_rows, a.P), b);
-  if (narrow) grid.x = std::min<int>(grid.x, std::max(1, 2 * 148 / b));
+  if (narrow) grid.x = std::min<int>(grid.x, std::max(1, 2 * sm_count() / b));
   if (narrow) {
-    cudaFuncSetAttribute(token_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (cudaError_t e = smem_optin(token_kernel<true>, int(smem))) return e;
     launch_seq(token_kernel<true>, grid, 256, smem, s, a);
   } else {
-    cudaFuncSetAttribute(token_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (cudaError_t e = smem_optin(token_kernel<false>, int(smem))) return e;
     launch_seq(token_kernel<false>, grid, 256, smem, s, a);
   }
   return cudaGetLastError();

@@ -351,17 +351,8 @@ bool token_tc_supported(const Dims& D) {
 
 cudaError_t launch_token_tc(const TokenTcArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(TokSmem) + 128;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(token_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  if (cudaError_t e = smem_optin(token_tc_kernel, int(smem))) return e;
+  const int sms = sm_count();
   const int P = 4 * (32 / a.nt);
   const int tiles = ((a.ns + P - 1) / P) * a.b;
   const int ctas = (tiles + kSlots - 1) / kSlots;

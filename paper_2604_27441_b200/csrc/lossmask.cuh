@@ -232,6 +232,11 @@ __device__ inline int lossmask_job(const nvrec_lossmask_job& job_in, int32_t* bl
   if (!err && rank_base != H.n_present) err = kBitmapCount;
   if (!err && H.kind > 1) err = kBadKind;
   __syncthreads();
+  // an undecodable frame (LOST_FRAME in the reference, receiver.py:244-248)
+  // recovers nothing: clear its wire bits so a recovery launch that consumes
+  // them (graphs run unconditionally) leaves the plane untouched
+  if (err && job.wire_bits)
+    for (int t = threadIdx.x; t < (job.grid_capacity + 7) / 8; t += blockDim.x) job.wire_bits[t] = 0;
   if (threadIdx.x == 0) {
     job.status[0] = err;
     job.status[1] = err ? 0 : *sh_flagged;

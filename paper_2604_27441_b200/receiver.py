@@ -18,9 +18,14 @@ receiver's P-frame finalisation (rgbdstream/receiver.py:211-274):
 Per frame time only the compressed bytes travel host -> device (codec header
 + assembled body, ~60-200 KB at 720p instead of a 2.8 MB plane), and the
 displayable plane comes back.  Decode errors (``UndecodableError`` in the
-reference, i.e. LOST_FRAME) are reported per stream by ``result``; a lost
-frame's slot then holds a partially decoded plane, exactly as the caller's
-fallback policy decides what to display.
+reference, i.e. LOST_FRAME, receiver.py:244-248) are reported per stream by
+``result``.  The reference then displays nothing and leaves its references
+alone; here every stream's ring advances together, so the lost frame's slot
+receives a copy of the newest displayable plane (the next P-frame decodes
+against the same plane as in the reference) and recovers nothing (its wire
+bits are cleared on the device).  The one deviation: the ring holds the
+newest plane twice instead of keeping its oldest reference for one more
+frame.
 """
 
 from __future__ import annotations

@@ -259,6 +259,14 @@ class RecoveryPipeline:
         self.ev_d2h[handle].synchronize()
         return self.host_out[handle].numpy()
 
+    def status(self, handle: int) -> np.ndarray:
+        """Per-stream loss-mask status of a step (0 = ok; else the header was
+        undecodable -- LOST_FRAME in the reference receiver, receiver.py:
+        244-248 -- and the kernel cleared that stream's wire bits, so its
+        plane was returned exactly as submitted)."""
+        self.ev_d2h[handle].synchronize()
+        return self.lm[handle].status[:self.n, 0].cpu().numpy()
+
 
 def recover_depth16(model, plane: np.ndarray, grid: np.ndarray, refs: list) -> np.ndarray:
     """16-bit depth extension of ``_recover`` (SPEC.md:74 calls 16-bit depth

@@ -73,7 +73,7 @@ def p_body(t):
 def i_shards(t):
     """Receiver._finalize_i inputs of an ``iframe`` trial: the n + r shard
     list (None = lost), padded to shard_len (receiver.py:185-191)."""
-    from paper_2604_27441_b200 import synth
+    from tools import synth
     data = blob(t["data"])
     n, r, L = t["n"], t["r"], t["L"]
     shards = [data[i * L:(i + 1) * L].ljust(L, b"\0") for i in range(n)]

@@ -11,6 +11,8 @@ Outputs (committed):
                                    (reference pkg/nvrec/src/nvrec/server.py:181-196)
   tests/golden/lossmask_golden.npz receiver+codec corruption masks
                                    (reference receiver.py:211-274, codec.py:260-321)
+  tests/golden/ssim_golden.npz     rgbdstream.metrics.ssim values
+                                   (reference metrics.py:41-72)
 
 Inputs are NOT stored: they are rebuilt from seeds by
 ``tests/golden_cases.py`` (and digests are stored to catch drift).
@@ -421,9 +423,22 @@ def gen_codec():
           "refs", len(refs), "errors", sum(1 for t in trials if t["err"]))
 
 
+def gen_ssim():
+    """rgbdstream.metrics.ssim (metrics.py:41-72) on seeded plane pairs."""
+    from golden_cases import SSIM_CASES, ssim_case
+    from rgbdstream.metrics import ssim
+    out = {}
+    for name in SSIM_CASES:
+        a, b = ssim_case(name)
+        out[name] = np.array(ssim(a, b), np.float64)
+        out[name + "__digest"] = np.array(digest(a, b))
+        print("ssim", name, a.shape, float(out[name]))
+    np.savez_compressed(os.path.join(HERE, "ssim_golden.npz"), **out)
+
+
 if __name__ == "__main__":
     torch.set_num_threads(8)
     import sys as _sys
-    which = _sys.argv[1:] or ["lossmask", "model", "recover", "baseline", "codec"]
+    which = _sys.argv[1:] or ["lossmask", "model", "recover", "baseline", "codec", "ssim"]
     for w in which:
         globals()["gen_" + w]()

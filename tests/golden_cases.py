@@ -102,3 +102,35 @@ def baseline_case(name):
     pix = np.repeat(np.repeat(grid, 16, 0), 16, 1)
     plane[pix] = 0
     return c, plane, grid, [frames[i] for i in range(nref)]
+
+
+# name -> (shape, noise std, seed) for the SSIM metric (rgbdstream
+# metrics.py:41-72): a textured plane against a noisy / shifted copy
+SSIM_CASES = {
+    "s_rgb_240x320_noise": ((240, 320, 3), 12.0, 51),
+    "s_depth_240x320_noise": ((240, 320), 4.0, 52),
+    "s_rgb_48x64_heavy": ((48, 64, 3), 60.0, 53),
+    "s_depth_17x23_odd": ((17, 23), 8.0, 54),
+    "s_depth_8x8_min": ((8, 8), 20.0, 55),
+    "s_rgb_32x32_identical": ((32, 32, 3), 0.0, 56),
+    "s_depth_720x1280_noise": ((720, 1280), 3.0, 57),
+}
+
+
+def ssim_case(name):
+    shape, std, seed = SSIM_CASES[name]
+    rng = np.random.default_rng(seed)
+    c = shape[2] if len(shape) == 3 else 1
+    a = textured_u8(rng, 1, shape[0], shape[1], c)[0]
+    if len(shape) == 2:
+        a = a[..., 0]
+    noise = rng.normal(0.0, std, a.shape) if std else 0.0
+    b = np.clip(np.rint(a.astype(np.float64) + noise), 0, 255).astype(np.uint8)
+    return a, b
+
+
+def recover_truth(name):
+    """The uncorrupted last frame of ``recover_case(name)`` (SSIM reference)."""
+    c, nref, h, w, ratio, seed = RECOVER_CASES[name]
+    rng = np.random.default_rng(seed)           # same draws as recover_case
+    return textured_u8(rng, nref + 1, h, w, c)[-1]

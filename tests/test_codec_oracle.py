@@ -30,7 +30,7 @@ def test_iframe_receiver_trials_and_parity():
     n = 0
     for t in trials("iframe"):
         data, shards = i_shards(t)
-        par = b"".join(s for s in __import__("paper_2604_27441_b200").synth.rs_parity(
+        par = b"".join(s for s in __import__("tools.synth").synth.rs_parity(
             data, t["n"], t["r"], t["L"]))
         assert sha(np.frombuffer(par, np.uint8)) == t["parity_digest"]
         try:
@@ -96,7 +96,8 @@ def test_rs_plan_host_matches_reference_reconstruct():
     """nvrec_rs_plan's reduced (m x n) decode coefficients reproduce the
     reference's full Gauss-Jordan reconstruction on every golden erasure
     pattern, plus random patterns up to n + r = 255."""
-    from paper_2604_27441_b200 import _native, synth
+    from paper_2604_27441_b200 import _native
+    from tools import synth
     lib = _native.load_library()
     cases = 0
     for t in trials("iframe"):

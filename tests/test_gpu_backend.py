@@ -74,7 +74,7 @@ def test_recovery_pipeline_matches_sequential_engine():
     receiver's ring semantics (recovered plane joins the ring)."""
     from paper_2604_27441_b200.lossmask import PFrameShards
     from paper_2604_27441_b200.recovery import RecoveryEngine, RecoveryPipeline
-    from paper_2604_27441_b200.synth import p_frame_shards
+    from tools.synth import p_frame_shards
     from oracle import lossmask as om
     ck, _ = _ck(3, 503)
     eng = RecoveryEngine(ck.build_model(), "fast")
@@ -107,7 +107,7 @@ def test_receiver_pipeline_matches_reference_receiver_chain():
     """GPU receiver (decode -> mask -> recover -> in-place ring) == the
     reference receiver's chain restated with the oracle decode
     (codec.py:260-321, receiver.py:222-269) and per-request engine calls."""
-    from paper_2604_27441_b200 import synth
+    from tools import synth
     from paper_2604_27441_b200.receiver import ReceiverPipeline
     from paper_2604_27441_b200.recovery import RecoveryEngine
     from oracle import codec as oc

@@ -118,7 +118,7 @@ def _scene(rng, h, w, c):
 @pytest.mark.parametrize("h,w,c,L,p", [(720, 1280, 3, 1024, 0.05), (720, 1280, 1, 512, 0.2),
                                        (1088, 1920, 3, 1024, 0.2), (480, 640, 1, 512, 0.5)])
 def test_large_stream_vs_oracle(h, w, c, L, p):
-    from paper_2604_27441_b200 import synth
+    from tools import synth
     cd = _codec()
     rng = np.random.default_rng(h + c)
     f0 = _scene(rng, h, w, c)
@@ -152,7 +152,7 @@ def test_large_stream_vs_oracle(h, w, c, L, p):
 
 @pytest.mark.parametrize("n,r,L", [(170, 85, 16384), (200, 55, 1001), (5, 3, 64), (1, 1, 4)])
 def test_rs_reconstruct_vs_oracle(n, r, L):
-    from paper_2604_27441_b200 import synth
+    from tools import synth
     cd = _codec()
     rng = np.random.default_rng(n * 7 + r)
     data = rng.integers(0, 256, n * L - 3, dtype=np.uint8).tobytes()

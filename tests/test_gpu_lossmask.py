@@ -63,7 +63,7 @@ def test_random_headers_vs_oracle():
     """Synthetic headers incl. inverted/empty block ranges (malformed offsets)
     and every loss pattern density: kernel == oracle, bit for bit."""
     lm = _lm()
-    from paper_2604_27441_b200.synth import p_frame_header, n_data_shards
+    from tools.synth import p_frame_header, n_data_shards
     rng = np.random.default_rng(77)
     frames, want = [], []
     for trial in range(300):
@@ -94,7 +94,7 @@ def test_random_headers_vs_oracle():
 def test_undecodable_headers_raise():
     lm = _lm()
     good, plen = None, None
-    from paper_2604_27441_b200.synth import p_frame_header
+    from tools.synth import p_frame_header
     good, plen = p_frame_header(np.random.default_rng(1), 64, 64, 1, 0.5)
     bad = [good[:10],                                          # truncated fixed part
            good[:6] + bytes([0]) + good[7:],                   # block 0

@@ -1,10 +1,13 @@
 """CUDA path vs the reference (golden fixtures) and the CPU oracle.
 
-Tolerances (north_star): max-abs <= 1e-2 on [0,1] outputs for the fast
-(bf16 tensor-core) path; the precise (fp32) path is held to 2e-5 against
-the reference's fp32 CPU forward (<= 1/65535 of full scale, the 16-bit
-depth "1 mm" bar).  u8 server outputs: <= 2 LSB fast (2/255 < 1e-2), <= 1
-LSB precise (a .5 quantisation edge can flip under fp32 re-association).
+Tolerances.  north_star: max-abs <= 1e-2 on [0,1] outputs, |dSSIM| <= 1e-3,
+<= 1 unit of 65535 on 16-bit depth.  The tests pin tighter regression
+bounds: the fast path (bf16/fp16 tensor-core operands, measured 2.6e-4 at
+720p) is held to 1e-3; the precise path (fp32-class: split bf16/fp16
+tensor-core operands, fp32 accumulation; measured ~3e-6) to 1.5e-5 <
+1/65535 against the reference's fp32 CPU forward.  u8 server outputs:
+<= 2 LSB fast (2/255 < 1e-2), <= 1 LSB precise (a .5 quantisation edge can
+flip under fp32 re-association).
 """
 
 import os
@@ -13,16 +16,18 @@ import numpy as np
 import pytest
 import torch
 
-from golden_cases import MODEL_CASES, RECOVER_CASES, model_case, recover_case
+from golden_cases import MODEL_CASES, RECOVER_CASES, model_case, recover_case, recover_truth
 from helpers import GOLDEN_DIR, block_grid, make_state, textured_u8
 from oracle import nvrec_forward, recover as oracle_recover
+from oracle.metrics import ssim
 
 pytestmark = pytest.mark.gpu
 
 MODEL = np.load(os.path.join(GOLDEN_DIR, "model_golden.npz"))
 RECOV = np.load(os.path.join(GOLDEN_DIR, "recover_golden.npz"))
 
-TOL = {"fast": 1e-2, "precise": 2e-5}
+TOL = {"fast": 1e-3, "precise": 1.5e-5}
+SSIM_TOL = 1e-3
 LSB = {"fast": 2, "precise": 1}
 
 
@@ -62,6 +67,12 @@ def test_recover_matches_reference_golden(name, precision):
     pix = np.repeat(np.repeat(grid, 16, 0), 16, 1)
     assert np.array_equal(got[~pix], plane[~pix])          # trusted pixels untouched
     assert np.abs(got.astype(int) - want.astype(int)).max() <= LSB[precision]
+    # north_star SSIM bar: SSIM against the uncorrupted frame, ours vs the
+    # reference's own _recover output (rgbdstream metrics.py:41-72)
+    truth = recover_truth(name)
+    truth = truth if got.ndim == 3 else truth[..., 0]
+    d = abs(ssim(truth, got) - ssim(truth, want))
+    assert d <= SSIM_TOL, d
 
 
 @pytest.mark.parametrize("c", [3, 1])
@@ -80,6 +91,8 @@ def test_recover_720p_vs_oracle(c):
         got = eng.recover(plane, grid, list(frames[:-1]))
         d = np.abs(got.astype(int) - want.astype(int))
         assert d.max() <= LSB[prec], (prec, d.max())
+        ds = abs(ssim(frames[-1], got) - ssim(frames[-1], want))
+        assert ds <= SSIM_TOL, (prec, ds)
 
 
 def test_pruned_server_path_equals_dense_forward():
@@ -212,7 +225,7 @@ def test_fast_path_runs_tensor_core_attention():
 
 
 def test_fast_vs_reference_error_budget_720p():
-    """bf16 tensor-core attention error at 1280x720 stays well inside 1e-2."""
+    """Module API at 1280x720: fast within 1e-3, precise within 1.5e-5."""
     arch = nvrec_forward.Arch()
     rng = np.random.default_rng(11)
     for c in (3, 1):
@@ -224,12 +237,12 @@ def test_fast_vs_reference_error_budget_720p():
                                             torch.from_numpy(mask).cuda()).cpu().numpy()
         err = np.abs(got - want)
         print("c=%d fast max-abs %.2e mean %.2e" % (c, err.max(), err.mean()))
-        assert err.max() <= 1e-2
+        assert err.max() <= TOL["fast"]
         got = _model(arch, c, state, "precise")(torch.from_numpy(stack).cuda(),
                                                torch.from_numpy(mask).cuda()).cpu().numpy()
         err = np.abs(got - want)
         print("c=%d precise max-abs %.2e (x65535 = %.3f)" % (c, err.max(), err.max() * 65535))
-        assert err.max() * 65535 <= 1.0
+        assert err.max() <= TOL["precise"]
 
 
 def _attn_mode_run(mode, path):

@@ -9,7 +9,7 @@ from oracle import lossmask as om
 from paper_2604_27441_b200 import Checkpoint, LossWeights, MaskedVideoModel, ModelConfig
 from paper_2604_27441_b200.lossmask import PFrameShards, grid_blocks
 from paper_2604_27441_b200.recovery import pack_grid, stack_slots
-from paper_2604_27441_b200.synth import GilbertElliott, n_data_shards, p_frame_header
+from tools.synth import GilbertElliott, n_data_shards, p_frame_header
 
 
 def test_config_mirror():
@@ -102,3 +102,41 @@ def test_cyclic_slot_ring_schedule():
             assert t - last_read[staged] >= nbuf
         for s in ring:
             last_read[s] = t
+
+
+def test_forward_value_errors_match_reference():
+    """pkg/nvrec/tests/test_nvrec_model.py:79-97: the reference raises
+    ValueError mentioning "channels", "patch" and "stack" (model.py:93-98),
+    before any compute -- so no GPU is needed to check them."""
+    import torch
+    from paper_2604_27441_b200 import MaskedVideoModel, ModelConfig
+    cfg = ModelConfig(k=1, tubelet_t=1, dim=16, layers=1, heads=2)
+    model = MaskedVideoModel(cfg, 3)
+    mask = torch.zeros(1, 16, 16, dtype=torch.bool)
+    with pytest.raises(ValueError, match="channels"):
+        model(torch.rand(1, 2, 1, 16, 16), mask)
+    with pytest.raises(ValueError, match="patch"):
+        model(torch.rand(1, 2, 3, 20, 16), torch.zeros(1, 20, 16, dtype=torch.bool))
+    with pytest.raises(ValueError, match="stack"):
+        model(torch.rand(1, 3, 3, 16, 16), mask)
+
+
+def test_u8_path_envelope_and_server_refusal():
+    from paper_2604_27441_b200 import Checkpoint, ModelConfig
+    from paper_2604_27441_b200.config import u8_path_unsupported
+    from paper_2604_27441_b200.server import RecoveryServer
+    assert u8_path_unsupported(ModelConfig()) is None
+    assert "patch" in u8_path_unsupported(ModelConfig(patch=8))
+    assert "dim" in u8_path_unsupported(ModelConfig(dim=24, heads=3))
+    ck = Checkpoint.random_init(ModelConfig(patch=8, dim=16, layers=1), 1, seed=0)
+    with pytest.raises(ValueError, match="patch"):
+        RecoveryServer(("127.0.0.1", 0), checkpoint_depth=ck)
+
+
+def test_request_size_from_header():
+    import struct
+    from paper_2604_27441_b200.server import MSG_REQUEST, ProtocolError, _request_bytes
+    head = struct.pack("<BBIHHB", MSG_REQUEST, 0, 7, 64, 32, 5)
+    assert _request_bytes(head) == 11 + (2 * 4 + 7) // 8 + 64 * 32 * 3 * 6
+    with pytest.raises(ProtocolError):
+        _request_bytes(struct.pack("<BBIHHB", MSG_REQUEST, 9, 7, 64, 32, 5))

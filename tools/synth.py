@@ -1,5 +1,8 @@
 """Synthetic workload generators for the benchmark and tests (no reference
-code needed on the GPU box).
+code needed on the GPU box).  WORKLOAD INFRASTRUCTURE, not product code:
+nothing in ``paper_2604_27441_b200/`` imports it; ``bench.py`` and
+``tests/`` use it to synthesise the sender side (encoded P-frames, shard
+plans, channel loss) that the recovery path consumes.
 
 * ``p_frame_header`` -- a codec P-frame header with the reference layout
   (codec.py:26,146-153: ``<BBHHBBIH`` + MSB-first present bitmap + u32
