@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define NVREC_ABI_VERSION 3
+#define NVREC_ABI_VERSION 4
 
 enum {
   NVREC_OK = 0,
@@ -50,10 +50,14 @@ enum {
 };
 
 /* Precision of the arithmetic on the forward path.
- *   NVREC_PREC_FAST:    bf16 tensor-core (tcgen05) attention, fp32
+ *   NVREC_PREC_FAST:    bf16/fp16 tensor-core (tcgen05) operands, fp32
  *                       accumulation/softmax/LN/GELU; RGB and u8 depth.
- *   NVREC_PREC_PRECISE: fp32 everywhere (CUDA-core SIMT); the 16-bit depth
- *                       mode (<= 1/65535 of full scale). */
+ *   NVREC_PREC_PRECISE: fp32-class: every tensor-core product from split bf16
+ *                       operands (a = hi + lo, hi*hi + hi*lo + lo*hi, fp32
+ *                       accumulation; ~16 significant bits per operand), all
+ *                       other arithmetic fp32; shapes outside the tensor-core
+ *                       envelope run fp32 CUDA-core kernels.  The 16-bit
+ *                       depth mode (<= 1/65535 of full scale). */
 enum { NVREC_PREC_FAST = 0, NVREC_PREC_PRECISE = 1 };
 
 /* Architecture fields of nvrec ModelConfig (config.py:14-19,35-41). */
@@ -227,6 +231,12 @@ enum {
 };
 int nvrec_profile_begin(void);
 int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages);
+
+/* Diagnostics: attention work items (query group x key split x sequence) the
+ * exact fix-up launch has recomputed on the current device since the process
+ * started (the speculative running max overflowed for them).  Synchronises
+ * the device. */
+int64_t nvrec_attn_fixup_items(void);
 
 #ifdef __cplusplus
 }

@@ -28,10 +28,11 @@ EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_model_destroy", "nvrec_model_load", "nvrec_workspace_bytes",
            "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask",
            "nvrec_profile_begin", "nvrec_profile_end", "nvrec_baseline_workspace_bytes",
-           "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct")
+           "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct",
+           "nvrec_attn_fixup_items")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
           "token", "baseline", "decode", "rs")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class NativeError(RuntimeError):
@@ -108,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_decode.argtypes = [vp, i32, i32, vp]
         lib.nvrec_rs_plan.argtypes = [i32, i32, vp, vp, vp, vp, ctypes.POINTER(i32)]
         lib.nvrec_rs_reconstruct.argtypes = [vp, i32, i32, i32, i32, vp]
+        lib.nvrec_attn_fixup_items.restype = i64
         lib.nvrec_profile_end.argtypes = [ctypes.POINTER(ctypes.c_float),
                                           ctypes.POINTER(i32), i32]
         for name in EXPORTS:
@@ -212,6 +214,15 @@ class NativeModel:
                                         None if out is None else out.data_ptr(),
                                         ws.data_ptr(), ws.numel(), prec, stream_ptr()))
         return out
+
+
+def attn_fixup_items() -> int:
+    """Attention work items recomputed by the exact fix-up so far (device-wide
+    counter, current device)."""
+    n = load_library().nvrec_attn_fixup_items()
+    if n < 0:
+        check(int(n))
+    return int(n)
 
 
 class StageProfile:

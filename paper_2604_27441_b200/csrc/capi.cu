@@ -171,6 +171,14 @@ struct WorkspaceLayout {
   size_t x, ao, q, k, v, qh, kh, vth, list, rank, count, part, redo, xh, total;
 };
 
+// Attention variant of a forward: 0 = fp32 SIMT (shapes outside the tensor-
+// core envelope), 1 = bf16 tensor cores (fast), 2 = split-bf16 tensor cores
+// (precise: hi*hi + hi*lo + lo*hi, fp32-class products).
+int attn_mode(const Dims& D, int precision) {
+  if (!nvrec::tc_supported(D)) return 0;
+  return precision == NVREC_PREC_FAST ? 1 : 2;
+}
+
 WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
   const int ns = (h / D.p) * (w / D.p);
   const int ns_pad = nvrec::round_up(ns, nvrec::kAttnQTile);
@@ -185,17 +193,18 @@ WorkspaceLayout layout_ws(const Dims& D, int b, int h, int w, int precision) {
   const size_t seqrows = size_t(b) * D.nt * D.heads * ns_pad * D.hd;
   L.x = take(tok * D.d * 4);
   L.ao = take(tok * D.d * 4);
-  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(D);
-  if (fast) {
-    L.xh = take(tok * D.d * 2);
-    L.qh = take(seqrows * 2);
-    L.kh = take(seqrows * 2);
-    L.vth = take(seqrows * 2);
+  const int am = attn_mode(D, precision);
+  if (am) {
+    L.xh = am == 1 ? take(tok * D.d * 2) : SIZE_MAX;
+    const size_t sz = seqrows * 2 * (am == 2 ? 2 : 1);   // x3: hi and lo
+    L.qh = take(sz);
+    L.kh = take(sz);
+    L.vth = take(sz);
     L.q = L.k = L.v = SIZE_MAX;
     L.part = take(size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads * ns * 36 * 4);
     // work items: query groups (>= one 128-query tile) x splits x sequences
-    // (+ the count)
-    L.redo = take((1 + size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads *
+    // (+ the count and the fix-up exit counter)
+    L.redo = take((2 + size_t(nvrec::kAttnMaxSplits) * b * D.nt * D.heads *
                    ((ns + nvrec::kAttnQTile - 1) / nvrec::kAttnQTile)) * 4);
   } else {
     L.q = take(seqrows * 4);
@@ -242,31 +251,34 @@ struct InPlace {
   const int32_t* frame_index = nullptr;
 };
 
-int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, bool fast,
+int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, int am,
                bool pruned, int h, int w, float* out_f32, uint8_t* out_u8,
                cudaStream_t s, InPlace ip = {}) {
   const Dims& D = m->D;
   const int b = A.b;
+  const bool fast = am == 1;
   nvrec::QkvDst dst{};
   dst.nt = D.nt; dst.ns = A.ns; dst.ns_pad = A.ns_pad; dst.d = D.d;
   dst.heads = D.heads; dst.hd = D.hd;
   dst.q = A.q; dst.k = A.k; dst.v = A.v; dst.qh = A.qh; dst.kh = A.kh; dst.vth = A.vth;
+  dst.x3 = am == 2;
   // arm the attention fix-up list once per forward (every fix-up launch
   // leaves it empty again)
-  if (fast && A.redo_list) CK(cudaMemsetAsync(A.redo_list, 0, sizeof(int), s), "memset");
+  if (am && A.redo_list) CK(cudaMemsetAsync(A.redo_list, 0, 2 * sizeof(int), s), "memset");
   for (int li = 0; li < D.layers; ++li) {
     const bool last = li == D.layers - 1;
     const bool prune_here = last && pruned;
     // block li's spatial attention: Q/K/V were written by the previous stage
     cudaError_t e;
     int splits = 1;
-    if (fast) {
+    if (am) {
       ProfScope ps(NVREC_STAGE_ATTN_TC, s);
       int nk = 1;
       // the SIMT token kernel (last block) merges key-split partials itself
-      const bool defer = last || !nvrec::token_tc_supported(D) || !m->W.tc.blk[li];
+      const bool defer = !fast || last || !nvrec::token_tc_supported(D) || !m->W.tc.blk[li];
       e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits,
-                                !defer);   // token_tc reads ao as fp16
+                                !defer,    // token_tc reads ao as fp16
+                                am == 2);
       ps.kernels(nk);
     } else {
       nvrec::AttnArgs aa{};
@@ -550,7 +562,7 @@ static nvrec::Act make_act(const nvrec_model* m, void* ws, const WorkspaceLayout
 static int embed_and_qkv0(const nvrec_model* m, nvrec::Act& A, bool u8, const float* stack,
                           int f, const uint8_t* pmask, const uint8_t* frames,
                           const int32_t* frame_index, int h, int w, bool pruned,
-                          cudaStream_t s) {
+                          int precision, cudaStream_t s) {
   const Dims& D = m->D;
   nvrec::EmbedArgs ea{};
   ea.D = D;
@@ -578,6 +590,7 @@ static int embed_and_qkv0(const nvrec_model* m, nvrec::Act& A, bool u8, const fl
   la.dst.rank = (pruned && D.layers == 1) ? A.rank : nullptr;
   la.dst.nt = D.nt; la.dst.ns = A.ns; la.dst.ns_pad = A.ns_pad; la.dst.d = D.d;
   la.dst.heads = D.heads; la.dst.hd = D.hd;
+  la.dst.x3 = attn_mode(D, precision) == 2;
   la.ns = A.ns;
   {
     ProfScope ps(NVREC_STAGE_LNQKV, s);
@@ -599,10 +612,10 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b, int32
   if (!stack || !mask || !out) return fail(NVREC_E_INVALID, "null tensor pointer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   nvrec::Act A = make_act(m, ws, L, b, h, w);
-  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
-  rc = embed_and_qkv0(m, A, false, stack, f, mask, nullptr, nullptr, h, w, false, s);
+  const int am = attn_mode(m->D, precision);
+  rc = embed_and_qkv0(m, A, false, stack, f, mask, nullptr, nullptr, h, w, false, precision, s);
   if (rc) return rc;
-  return run_blocks(m, A, L, fast, false, h, w, out, nullptr, s);
+  return run_blocks(m, A, L, am, false, h, w, out, nullptr, s);
 }
 
 int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
@@ -619,7 +632,8 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   if (n_slots < 1) return fail(NVREC_E_INVALID, "n_slots must be >= 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   nvrec::Act A = make_act(m, ws, L, b, h, w);
-  const bool fast = precision == NVREC_PREC_FAST && nvrec::tc_supported(m->D);
+  const int am = attn_mode(m->D, precision);
+  const bool fast = am == 1;
   const int nbytes = (A.ns + 7) / 8;
   cudaError_t e;
   {
@@ -650,7 +664,8 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     }
     if (e2 != cudaSuccess) return cuda_fail(e2, "embed_tc launch");
   } else {
-    rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true, s);
+    rc = embed_and_qkv0(m, A, true, nullptr, 0, nullptr, frames, frame_index, h, w, true,
+                        precision, s);
     if (rc) return rc;
   }
   if (!out) {
@@ -659,7 +674,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     InPlace ip;
     ip.frames = const_cast<uint8_t*>(frames);
     ip.frame_index = frame_index;
-    return run_blocks(m, A, L, fast, true, h, w, nullptr, nullptr, s, ip);
+    return run_blocks(m, A, L, am, true, h, w, nullptr, nullptr, s, ip);
   }
   // the merge base (corrupted plane) is copied only after the embedding has
   // read every stacked frame, so `out` may alias a reference slot (a ring
@@ -669,7 +684,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "copy launch");
-  return run_blocks(m, A, L, fast, true, h, w, nullptr, out, s);
+  return run_blocks(m, A, L, am, true, h, w, nullptr, out, s);
 }
 
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream) {
@@ -759,6 +774,12 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
   }
   if (e != cudaSuccess) return cuda_fail(e, "baseline launch");
   return 0;
+}
+
+int64_t nvrec_attn_fixup_items(void) {
+  const int64_t n = nvrec::attn_fixup_items();
+  if (n < 0) return fail(NVREC_E_CUDA, "reading the fix-up counter failed");
+  return n;
 }
 
 int nvrec_profile_begin(void) {

@@ -29,6 +29,19 @@
 // The exponentials bind (head_dim 32 gives 128 MMA FLOP per exp, SURVEY.md
 // 8d): MUFU ex2 for most pairs, the FMA-pipe polynomial for one pair in
 // kPolyOf4 of each four.
+//
+// kX3 (the precise path): fp32-class products from split bf16 operands,
+// a = a_hi + a_lo with a_hi = bf16(a), a_lo = bf16(a - a_hi) (16 significant
+// bits), every product formed as hi*hi + hi*lo + lo*hi with fp32
+// accumulation:
+//   Q, K  [seq][ns_pad][64] bf16, columns 0-31 hi, 32-63 lo (128-byte rows,
+//         SWIZZLE_128B): S = Qh Kh^T + Qh Kl^T + Ql Kh^T = six K16 MMAs
+//   V^T   [seq][64][ns_pad], rows 0-31 hi, 32-63 lo
+//   P     split by the softmax warps: P_hi pairs over S columns 0-31, P_lo
+//         pairs over 32-63; O'(j) = Ph Vh + Ph Vl + Pl Vh (12 K16 MMAs) into
+//         a separate 32-column accumulator per query tile.
+// Key tiles are 64 keys (the split P fills its S buffer), all exponentials on
+// MUFU (ex2.approx.f32, rel. error ~2^-22).  TMEM: QT x (2 x 64 + 32) columns.
 #include <cstdlib>
 #include <type_traits>
 
@@ -48,6 +61,20 @@ constexpr int kHd = 32;
 constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
 constexpr int kStages = 6;
+// per-variant geometry (kX3: split-bf16 precise path, see the header)
+template <bool X3> struct Geo {
+  static constexpr int TK = X3 ? 64 : 128;              // keys per tile
+  static constexpr uint32_t Row = X3 ? 128 : 64;        // bytes per Q/K row
+  static constexpr uint32_t QBytes = kTileQ * Row;
+  static constexpr uint32_t KBytes = TK * Row;
+  static constexpr uint32_t VBytes = 8192;              // V^T tile: 32 dims x 128 keys | 64 rows x 64 keys
+  static constexpr uint32_t Sw = X3 ? 2u /*kSwizzle128B*/ : 4u /*kSwizzle64B*/;
+  static constexpr uint32_t Sbo = X3 ? 1024 : 512;
+};
+template <bool X3, int QT> __host__ __device__ constexpr int stages_for() { return X3 && QT == 1 ? 5 : kStages; }
+template <bool X3, int QT> __host__ __device__ constexpr uint32_t tmem_cols() {
+  return X3 ? (QT == 2 ? 512u : 256u) : uint32_t(QT * 256);
+}
 // QT = query tiles per CTA: 2 for dense launches (one CTA per SM, all 512 TMEM
 // columns); 1 for pruned launches (a handful of masked-patch queries per
 // sequence: latency-bound, so two CTAs share an SM and the key range is split
@@ -69,13 +96,14 @@ constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buf
 constexpr float kSlackSum = 256.f;                     // speculative-max headroom: row sum of P
 static_assert(2 * 2 * kTileK <= 512, "TMEM budget");
 
-template <int QT>
+template <int QT, bool X3 = false>
 struct __align__(1024) Smem {
-  uint8_t v[kStages][kVBytes];      // 1024-aligned (SWIZZLE_128B atoms)
-  uint8_t q[QT][kQBytes];           // 512-aligned (SWIZZLE_64B atoms)
-  uint8_t k[kStages][kKBytes];
+  static constexpr int NS = stages_for<X3, QT>();
+  uint8_t v[NS][Geo<X3>::VBytes];   // 1024-aligned (SWIZZLE_128B atoms)
+  uint8_t q[QT][Geo<X3>::QBytes];   // 512/1024-aligned (SWIZZLE_64B/128B atoms)
+  uint8_t k[NS][Geo<X3>::KBytes];
   uint64_t q_full;
-  uint64_t kv_full[kStages], kv_empty[kStages];
+  uint64_t kv_full[NS], kv_empty[NS];
   uint64_t s_full[QT][2], p_full[QT], pv_full[QT], o_read[QT], done;
   int redo[3];                      // per group iteration (mod 3): speculative max overflowed
   uint32_t tmem_base;
@@ -93,14 +121,30 @@ struct TcArgs {
   int* redo_list;     // [0] = count, then work items whose speculative max overflowed
   float scale_log2;
 };
-constexpr int kPart = 36;                              // 32 output dims, m, l, 2 pad (16 B rows)
+constexpr int kPart = 36;
+constexpr int kFixCtas = 32;                           // exact fix-up grid (grid-stride list walk)
+__device__ unsigned long long g_fix_items;             // diagnostics: items redone so far                              // 32 output dims, m, l, 2 pad (16 B rows)
 
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 * t + (j & 1)) * kTileK); }
+template <bool X3 = false>
+__device__ __forceinline__ uint32_t buf_col(int t, int j) {
+  return uint32_t((2 * t + (j & 1)) * Geo<X3>::TK);
+}
+// O'(j) of query tile t: inside its S buffer (fast) or its own 32 columns (kX3)
+template <bool X3, int QT>
+__device__ __forceinline__ uint32_t o_col(int t, int j) {
+  return X3 ? uint32_t(2 * QT * Geo<X3>::TK + 32 * t) : buf_col<X3>(t, j) + kColOp;
+}
+// bf16 hi/lo split of a pair: hi = bf16(p), lo = bf16(p - hi)
+__device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16(x, y);
+  const float2 h = unpack_bf16(hi);
+  lo = pack_bf16(x - h.x, y - h.y);
+}
 
 // Work item = (query group, key split, sequence), it = (group*splits + split)*seqs + seq.
 // kMulti: the CTA may loop over several items (pruned launches step through a
@@ -109,21 +153,44 @@ __device__ __forceinline__ uint32_t buf_col(int t, int j) { return uint32_t((2 *
 // kExact: exact per-tile maxima (the fix-up); otherwise the speculative
 // running max, and a CTA whose exponent overflowed records its item for the
 // fix-up launch that follows on the same stream.
-template <bool kMulti, bool kExact, bool kList, int kQT>
+template <bool kMulti, bool kExact, bool kList, int kQT, bool kX3 = false>
 __global__ void __launch_bounds__(threads_for(kQT), kQT == 1 ? 2 : 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
+  using G = Geo<kX3>;
+  constexpr int TK = G::TK;
+  constexpr int NS = stages_for<kX3, kQT>();
   pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem<kQT>& sm = *reinterpret_cast<Smem<kQT>*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
+  Smem<kQT, kX3>& sm = *reinterpret_cast<Smem<kQT, kX3>*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkv_all = (a.ns + kTileK - 1) / kTileK;
-  const int n_list = kList ? a.redo_list[0] : 0;
-  if (kList && n_list == 0) return;                       // nothing overflowed (uniform)
+  const int nkv_all = (a.ns + TK - 1) / TK;
+  const int n_list = kList ? *(volatile int*)a.redo_list : 0;
+  // fix-up launch: the last CTA to leave re-arms the list (count and exit
+  // counter back to 0) once every CTA has read the count
+  auto fix_exit = [&]() {
+    if (kList && threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.redo_list + 1, 1) == int(gridDim.x) - 1) {
+        a.redo_list[0] = 0;
+        a.redo_list[1] = 0;
+      }
+    }
+  };
+  if (kList && n_list > 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&g_fix_items, (unsigned long long)n_list);
+  if (kList && n_list == 0) {                             // nothing overflowed (uniform)
+    __syncthreads();
+    fix_exit();
+    return;
+  }
   // the k-th work item of this CTA, or -1 when done
   auto item_at = [&](int k) -> int {
-    if (kList) return k < n_list ? a.redo_list[1 + k] : -1;
+    if (kList) {
+      const int i = int(blockIdx.x) + k * int(gridDim.x);
+      return i < n_list ? a.redo_list[2 + i] : -1;
+    }
     if (!kMulti && k > 0) return -1;
     return int(blockIdx.x) + k * int(gridDim.x);
   };
@@ -149,7 +216,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     sm.redo[0] = (a.mode == 2 && !kExact) ? 1 : 0;   // mode 2: the first item is redone
     sm.redo[1] = sm.redo[2] = 0;
     mbar_init(&sm.q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
     }
@@ -165,7 +232,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
   }
-  if (warp == 0) tmem_alloc<kQT * 256>(&sm.tmem_base);
+  if (warp == 0) tmem_alloc<tmem_cols<kX3, kQT>()>(&sm.tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -199,56 +266,79 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       // ---------------------------------------------------------- TMA producer
       if (lane == 0) {
         sm.redo[(gq + 1) % 3] = 0;                 // slot of iteration gq+1 (last read at gq-2)
-        mbar_expect_tx(&sm.q_full, ntq * kQBytes);
+        mbar_expect_tx(&sm.q_full, ntq * G::QBytes);
         for (int t = 0; t < ntq; ++t)
           tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
         for (int j = 0; j < nkv; ++j) {
-          const int g = gkv + j, s = g % kStages;
-          mbar_wait(&sm.kv_empty[s], ((g / kStages) & 1) ^ 1);
-          mbar_expect_tx(&sm.kv_full[s], kKBytes + kVBytes);
-          const int key0 = (j0 + j) * kTileK;
+          const int g = gkv + j, s = g % NS;
+          mbar_wait(&sm.kv_empty[s], ((g / NS) & 1) ^ 1);
+          mbar_expect_tx(&sm.kv_full[s], G::KBytes + G::VBytes);
+          const int key0 = (j0 + j) * TK;
           tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, key0, seq);
           tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], key0, 0, seq);
-          tma_load_3d(sm.v[s] + kVBytes / 2, &tm_v, &sm.kv_full[s], key0 + 64, 0, seq);
+          if (!kX3) tma_load_3d(sm.v[s] + G::VBytes / 2, &tm_v, &sm.kv_full[s], key0 + 64, 0, seq);
         }
       }
     } else if (warp == kMma) {
       // ---------------------------------------------------------- MMA issuer
       if (lane == 0) {
-        uint64_t qdesc[kQT][2];
+        constexpr int QK = kX3 ? 4 : 2;            // K16 chunks per Q/K row
+        uint64_t qdesc[kQT][QK];
         for (int t = 0; t < kQT; ++t)
-          for (int kk = 0; kk < 2; ++kk)
-            qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, 512, kSwizzle64B);
+          for (int kk = 0; kk < QK; ++kk)
+            qdesc[t][kk] = sdesc(smem_u32(sm.q[t]) + kk * 32, G::Sbo, G::Sw);
+        constexpr uint32_t idS = idesc_bf16(128, TK);
         mbar_wait(&sm.q_full, gq & 1);
         for (int j = 0; j <= nkv; ++j) {
           if (j < nkv) {
             // S_t(j) into buf[t][j%2] once O'(j-2) there has been folded
-            const int g = gkv + j, s = g % kStages;
-            mbar_wait_fast(&sm.kv_full[s], (g / kStages) & 1);
+            // (kX3: once P(j-2) was read by PV(j-2), issued earlier in order)
+            const int g = gkv + j, s = g % NS;
+            mbar_wait_fast(&sm.kv_full[s], (g / NS) & 1);
             tc_fence_after();
             const uint32_t kb = smem_u32(sm.k[s]);
             for (int t = 0; t < ntq; ++t) {
-              if (j >= 2) {
-                mbar_wait_fast(&sm.o_read[t], (go[t] + j - 2) & 1);
-                tc_fence_after();
+              const uint32_t sc = tmem + buf_col<kX3>(t, gs[t] + j);
+              if constexpr (kX3) {
+                // hi.hi + hi.lo + lo.hi: (Q chunk, K chunk) over the 128-byte rows
+                constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kb_[6] = {0, 1, 2, 3, 0, 1};
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+                  mma_ss(sc, qdesc[t][qa[u]], sdesc(kb + kb_[u] * 32, G::Sbo, G::Sw), idS, u);
+              } else {
+                if (j >= 2) {
+                  mbar_wait_fast(&sm.o_read[t], (go[t] + j - 2) & 1);
+                  tc_fence_after();
+                }
+                for (int kk = 0; kk < 2; ++kk)
+                  mma_ss(sc, qdesc[t][kk], sdesc(kb + kk * 32, G::Sbo, G::Sw), idS, kk);
               }
-              for (int kk = 0; kk < 2; ++kk)
-                mma_ss(tmem + buf_col(t, gs[t] + j), qdesc[t][kk],
-                       sdesc(kb + kk * 32, 512, kSwizzle64B), kIdescS, kk);
               mma_commit(&sm.s_full[t][(gs[t] + j) & 1]);
             }
           }
           if (j >= 1) {
             // O'_t(j-1) = P_t(j-1) V_{j-1}: M128 N32, 16 keys per step
-            const int jp = j - 1, sp = (gkv + jp) % kStages;
+            const int jp = j - 1, sp = (gkv + jp) % NS;
             const uint32_t vb = smem_u32(sm.v[sp]);
             for (int t = 0; t < ntq; ++t) {
               mbar_wait_fast(&sm.p_full[t], (gs[t] + jp) & 1);
               tc_fence_after();
-              const uint32_t bc = tmem + buf_col(t, gs[t] + jp);
-              for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
-                const uint32_t addr = vb + (kk >> 2) * (kVBytes / 2) + (kk & 3) * 32;
-                mma_ts(bc + kColOp, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+              const uint32_t bc = tmem + buf_col<kX3>(t, gs[t] + jp);
+              const uint32_t oc = tmem + o_col<kX3, kQT>(t, gs[t] + jp);
+              if constexpr (kX3) {
+                // Ph Vh + Ph Vl + Pl Vh; V^T rows 32-63 (lo) sit 4 KB after hi
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint32_t vh = vb + kk * 32;
+                  mma_ts(oc, bc + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, kk);
+                  mma_ts(oc, bc + kk * 8, sdesc(vh + 4096, 1024, kSwizzle128B), kIdescPV, 1);
+                  mma_ts(oc, bc + 32 + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
+                }
+              } else {
+                for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
+                  const uint32_t addr = vb + (kk >> 2) * (G::VBytes / 2) + (kk & 3) * 32;
+                  mma_ts(oc, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+                }
               }
               mma_commit(&sm.pv_full[t]);
             }
@@ -274,7 +364,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     tc_fence_after();
     if (!kExact && warp == kProducer && lane == 0 && sm.redo[gq_done % 3] != 0) {
       const int idx = atomicAdd(a.redo_list, 1);     // overflowed: exact fix-up later
-      a.redo_list[1 + idx] = it;
+      a.redo_list[2 + idx] = it;
     }
   }
   } else {
@@ -308,6 +398,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       const bool rows_live = q0 + t * kTileQ + quarter * 32 < nq;
       const int gst = gs[t];
       const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
+      // fold O'(g) into the register-resident output
+      auto fold = [&](int g) {
+        mbar_wait(&sm.pv_full[t], g & 1);
+        tc_fence_after();
+        uint32_t ov[32];
+        tmem_ld32(tmem + lane_off + o_col<kX3, kQT>(t, g), ov);
+        tmem_wait_ld();
+        const float2 ap = make_float2(a_prev, a_prev);
+#pragma unroll
+        for (int e = 0; e < kHd / 2; ++e)
+          o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
+                                               __uint_as_float(ov[2 * e + 1])));
+      };
       // the key-tile loop, specialised for speculative / exact maxima
       // (Z: counters known to be zero -- the single speculative pass of a
       // dense CTA -- so buffer/phase arithmetic folds at compile time)
@@ -317,16 +420,53 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         const int gst0 = Z ? 0 : gst;
         for (int j = 0; j < jend; ++j) {
           const int g = gst0 + j;
-          const uint32_t t_s = tmem + lane_off + buf_col(t, g);
+          const uint32_t t_s = tmem + lane_off + buf_col<kX3>(t, g);
           mbar_wait(&sm.s_full[t][g & 1], (g >> 1) & 1);
           tc_fence_after();
-          const int valid = a.ns - (j0 + j) * kTileK;   // keys of this tile that exist
+          const int valid = a.ns - (j0 + j) * TK;   // keys of this tile that exist
           // Running max: exact for the first key tile (pass 1), speculative
           // afterwards -- P is computed against the running max while the
           // tile's own max is tracked on the side; only a row whose max grew by
           // more than kSlack (P > 2^kSlack) rescales its stored P by an exact
           // power of two.  Softmax is shift-invariant, so this is the same sum.
           float mn = m;
+          float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          if constexpr (kX3) {
+            // one 64-key chunk: S -> P = 2^(s*scale - mn) (MUFU) -> P_hi/P_lo
+            // pairs over the S columns; then O'(j-1) is folded
+            if (rows_live) {
+              uint32_t r[64];
+              tmem_ld32(t_s, r);
+              tmem_ld32(t_s + 32, r + 32);
+              tmem_wait_ld();
+              if (valid < TK) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c)
+                  if (c >= valid) r[c] = __float_as_uint(-INFINITY);
+              }
+              if (j == 0 || EX) {
+                float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(r[c]));
+                mn = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2);
+              }
+              const float2 nm2 = make_float2(-mn, -mn);
+              uint32_t pl[32];
+#pragma unroll
+              for (int c = 0; c < 64; c += 2) {
+                const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                       sc2, nm2);
+                const float2 p = make_float2(ex2(v.x), ex2(v.y));
+                sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+                split_bf16(p.x, p.y, r[c >> 1], pl[c >> 1]);   // r[c/2] already consumed
+              }
+              tmem_st16(t_s, r);
+              tmem_st16(t_s + 16, r + 16);
+              tmem_st16(t_s + 32, pl);
+              tmem_st16(t_s + 48, pl + 16);
+            }
+            if (j > 0) fold(g - 1);
+          } else {
           if ((j == 0 || EX) && rows_live) {
             float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   #pragma unroll
@@ -345,7 +485,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
           // already-consumed S columns (chunk h2 reads S[64h2, 64h2+64) and
           // writes P pairs to columns [32h2, 32h2+32)); O'(j-1) is folded
           // between the two halves and its buffer handed back for S(j+1)
-          float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           const float2 nm2 = make_float2(-mn, -mn);
   #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {             // two 32-column chunks per wait
@@ -380,25 +519,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             tmem_st16(t_s + 32 * h2 + 16, pk + 16);
             }
             if (h2 == 0 && j > 0) {
-              mbar_wait(&sm.pv_full[t], (g - 1) & 1);
-              tc_fence_after();
-              uint32_t ov[32];
-              tmem_ld32(tmem + lane_off + buf_col(t, g - 1) + kColOp, ov);
-              tmem_wait_ld();
-              const float2 ap = make_float2(a_prev, a_prev);
-  #pragma unroll
-              for (int e = 0; e < kHd / 2; ++e)
-                o2[e] = ffma2(o2[e], ap, make_float2(__uint_as_float(ov[2 * e]),
-                                                     __uint_as_float(ov[2 * e + 1])));
+              fold(g - 1);
               tc_fence_before();
               mbar_arrive(&sm.o_read[t]);
             }
+          }
           }
           float2 sums = fadd2(sum2[0], sum2[1]);
           float tsum = sums.x + sums.y;
           if (!EX && j > 0 && __any_sync(0xffffffffu, !(tsum <= kSlackSum))) {
             // rare: the row sum exceeds 2^kSlack, so some p may too -- rescale
             // this row's P (and its sum) by 2^-k, k = ceil(log2 max p), exact
+            // (kX3: P_hi over columns 0-31 sets the max, P_lo scales alike)
             tmem_wait_st();
             uint32_t pk[2][32];
             float pmax = 0.f;
@@ -406,6 +538,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
             for (int h2 = 0; h2 < 2; ++h2) {
               tmem_ld32(t_s + 32 * h2, pk[h2]);
               tmem_wait_ld();
+              if (kX3 && h2 == 1) continue;
   #pragma unroll
               for (int c = 0; c < 32; ++c) {
                 const float2 pv = unpack_bf16(pk[h2][c]);
@@ -447,7 +580,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_wait(&sm.pv_full[t], g & 1);          // final O'
         tc_fence_after();
         uint32_t ov[32];
-        tmem_ld32(tmem + lane_off + buf_col(t, g) + kColOp, ov);
+        tmem_ld32(tmem + lane_off + o_col<kX3, kQT>(t, g), ov);
         tmem_wait_ld();
         float o[kHd];
 #pragma unroll
@@ -505,8 +638,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<kQT * 256>(tmem);
-  if (kList && threadIdx.x == 0) a.redo_list[0] = 0;      // single fix-up CTA: re-arm
+  if (warp == 0) tmem_dealloc<tmem_cols<kX3, kQT>()>(tmem);
+  fix_exit();
   pdl_trigger();
 }
 
@@ -571,20 +704,42 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 
 bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
+int64_t attn_fixup_items() {
+  unsigned long long v = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpyFromSymbol(&v, g_fix_items, sizeof v) != cudaSuccess)
+    return -1;
+  return int64_t(v);
+}
+
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
-                           int* n_kernels, bool defer_combine, int* splits_out, bool ao_half) {
+                           int* n_kernels, bool defer_combine, int* splits_out, bool ao_half,
+                           bool x3) {
   const int seqs = A.b * D.nt * D.heads;
   CUtensorMap tq, tk, tv;
-  const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
-  // Q/K: [seq][ns_pad][32] bf16 viewed (32, ns, seq); rows >= ns read as zero
-  if (!make_map_3d(&tq, A.qh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileQ,
-                   CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map_3d(&tk, A.kh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileK,
-                   CU_TENSOR_MAP_SWIZZLE_64B) ||
-      // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 64-key boxes (128 B rows)
-      !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 64, kHd,
-                   CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
+  if (!x3) {
+    const uint64_t row_b = kHd * 2, seq_b = uint64_t(A.ns_pad) * kHd * 2;
+    // Q/K: [seq][ns_pad][32] bf16 viewed (32, ns, seq); rows >= ns read as zero
+    if (!make_map_3d(&tq, A.qh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileQ,
+                     CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_map_3d(&tk, A.kh, kHd, A.ns, seqs, row_b, seq_b, kHd, kTileK,
+                     CU_TENSOR_MAP_SWIZZLE_64B) ||
+        // V^T: [seq][32][ns_pad] viewed (ns, 32, seq), 64-key boxes (128 B rows)
+        !make_map_3d(&tv, A.vth, A.ns, kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b, 64, kHd,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  } else {
+    // split operands: Q/K [seq][ns_pad][64] (hi | lo) as (64, ns, seq), 128-byte
+    // rows; V^T [seq][64][ns_pad] (hi rows | lo rows) as (ns, 64, seq)
+    const uint64_t row_b = 2 * kHd * 2, seq_b = uint64_t(A.ns_pad) * 2 * kHd * 2;
+    if (!make_map_3d(&tq, A.qh, 2 * kHd, A.ns, seqs, row_b, seq_b, 2 * kHd, kTileQ,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map_3d(&tk, A.kh, 2 * kHd, A.ns, seqs, row_b, seq_b, 2 * kHd, Geo<true>::TK,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_map_3d(&tv, A.vth, A.ns, 2 * kHd, seqs, uint64_t(A.ns_pad) * 2, seq_b,
+                     Geo<true>::TK, 2 * kHd, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
   TcArgs ta;
   ta.ao = A.ao;
   ta.ao_half = ao_half;
@@ -597,17 +752,6 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.seqs = seqs;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
   const int sms = sm_count();
-  {
-    const int s2 = int(sizeof(Smem<2>) + 1024), s1 = int(sizeof(Smem<1>) + 1024);
-    cudaError_t e;
-    if ((e = smem_optin(attn_tc_kernel<false, false, false, 2>, s2)) != cudaSuccess ||
-        (e = smem_optin(attn_tc_kernel<true, true, false, 2>, s2)) != cudaSuccess ||
-        (e = smem_optin(attn_tc_kernel<true, true, true, 2>, s2)) != cudaSuccess ||
-        (e = smem_optin(attn_tc_kernel<true, false, false, 1>, s1)) != cudaSuccess ||
-        (e = smem_optin(attn_tc_kernel<true, true, false, 1>, s1)) != cudaSuccess ||
-        (e = smem_optin(attn_tc_kernel<true, true, true, 1>, s1)) != cudaSuccess)
-      return e;
-  }
   // Dense launch: two query tiles per CTA, one CTA per SM (all of TMEM).  A
   // pruned launch (compact masked-patch queries, count on the device): one
   // query tile per CTA, two CTAs per SM, sized for one query group per
@@ -615,7 +759,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   // range (flash-decoding partials merged by attn_combine_kernel) so every
   // SM slot works.
   const int qt = count ? 1 : 2, per_sm = count ? 2 : 1;
-  const int nkv = ceil_div(A.ns, kTileK);
+  const int nkv = ceil_div(A.ns, x3 ? Geo<true>::TK : kTileK);
   ta.groups = count ? 1 : ceil_div(A.ns, qt * kTileQ);
   int best = 1;
   double best_t = 1e30;
@@ -639,23 +783,38 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   ta.mode = mode;
   ta.redo_list = A.redo_list;
   const dim3 grid(ta.groups * seqs * ta.splits);
-  auto run = [&](auto qt_tag) {
+  cudaError_t err = cudaSuccess;
+  auto run = [&](auto qt_tag, auto x3_tag) {
     constexpr int QT = decltype(qt_tag)::value;
+    constexpr bool X3 = decltype(x3_tag)::value;
     const int nth = threads_for(QT);
-    const size_t smem = sizeof(Smem<QT>) + 1024;
+    const size_t smem = sizeof(Smem<QT, X3>) + 1024;
+    auto k_exact = attn_tc_kernel<true, true, false, QT, X3>;
+    auto k_spec = attn_tc_kernel<QT == 1, false, false, QT, X3>;
+    auto k_fix = attn_tc_kernel<true, true, true, QT, X3>;
+    if ((err = smem_optin(k_exact, int(smem))) != cudaSuccess ||
+        (err = smem_optin(k_spec, int(smem))) != cudaSuccess ||
+        (err = smem_optin(k_fix, int(smem))) != cudaSuccess)
+      return;
     if (mode == 1 || !A.redo_list) {
       // exact maxima throughout (tests), or no fix-up list available
-      launch_seq(attn_tc_kernel<true, true, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
+      launch_seq(k_exact, grid, nth, smem, s, tq, tk, tv, ta);
     } else {
-      if constexpr (QT == 1) launch_seq(attn_tc_kernel<true, false, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
-      else launch_seq(attn_tc_kernel<false, false, false, QT>, grid, nth, smem, s, tq, tk, tv, ta);
-      // exact fix-up of the (rare) items whose speculative exponent overflowed;
-      // one CTA, exits at once when the list is empty, re-arms the list count
-      launch_pdl(attn_tc_kernel<true, true, true, QT>, 1, nth, smem, s, tq, tk, tv, ta);
+      launch_seq(k_spec, grid, nth, smem, s, tq, tk, tv, ta);
+      // exact fix-up of the (rare) items whose speculative exponent overflowed:
+      // a grid-stride walk of the list; every CTA exits at once when it is
+      // empty, and the last CTA out re-arms the list
+      launch_pdl(k_fix, kFixCtas, nth, smem, s, tq, tk, tv, ta);
     }
   };
-  if (qt == 1) run(std::integral_constant<int, 1>{});
-  else run(std::integral_constant<int, 2>{});
+  if (qt == 1) {
+    if (x3) run(std::integral_constant<int, 1>{}, std::true_type{});
+    else run(std::integral_constant<int, 1>{}, std::false_type{});
+  } else {
+    if (x3) run(std::integral_constant<int, 2>{}, std::true_type{});
+    else run(std::integral_constant<int, 2>{}, std::false_type{});
+  }
+  if (err != cudaSuccess) return err;
   const bool combine = ta.splits > 1 && !defer_combine;
   if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (combine ? 1 : 0);
   if (splits_out) *splits_out = ta.splits;

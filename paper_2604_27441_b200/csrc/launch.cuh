@@ -107,10 +107,13 @@ cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index,
 cudaError_t launch_token(const TokenArgs& a, int b, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_simt(const AttnArgs& a, int b, int max_rows, cudaStream_t s);
 // defer_combine: the consumer merges key-split partials itself (token_kernel);
-// *splits_out receives the split count (1 = ao written directly)
+// *splits_out receives the split count (1 = ao written directly); x3: the
+// precise path's split-bf16 operand layouts (QkvDst::x3)
 cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaStream_t s,
                            int* n_kernels = nullptr, bool defer_combine = false,
-                           int* splits_out = nullptr, bool ao_half = false);
+                           int* splits_out = nullptr, bool ao_half = false,
+                           bool x3 = false);
+int64_t attn_fixup_items();   // -1 on a CUDA error
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,

@@ -160,10 +160,12 @@ __device__ __forceinline__ void tile_layernorm(const float* in, int ldi, float* 
 // Scatter one qkv feature (model.py:37: reshape(b, t, 3, heads, hd)) of the
 // token (b, it, s) into the spatial-attention operand layouts.
 struct QkvDst {
-  float* q; float* k; float* v;                     // precise (fp32) layouts
-  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;  // fast (bf16)
+  float* q; float* k; float* v;                     // SIMT attention (fp32) layouts
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;  // tensor-core layouts
   const int* rank;   // non-null: Q rows are compact (pruned consumer block)
   int nt, ns, ns_pad, d, heads, hd;
+  int x3;            // tensor-core precise path: bf16 hi/lo split, Q/K rows
+                     // [hi(hd) | lo(hd)], V^T rows hi 0..hd-1, lo hd..2hd-1
 };
 
 __device__ __forceinline__ void qkv_store(const QkvDst& o, int b, int it, int s, int n, float v) {
@@ -176,7 +178,18 @@ __device__ __forceinline__ void qkv_store(const QkvDst& o, int b, int it, int s,
     row = o.rank[b * o.ns + s];
     if (row < 0) return;
   }
-  if (o.qh) {
+  if (o.qh && o.x3) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+    if (which < 2) {
+      __nv_bfloat16* r = (which == 0 ? o.qh : o.kh) + (seq * o.ns_pad + row) * 2 * o.hd;
+      r[e] = hi;
+      r[o.hd + e] = lo;
+    } else {
+      o.vth[(seq * 2 * o.hd + e) * o.ns_pad + row] = hi;
+      o.vth[(seq * 2 * o.hd + o.hd + e) * o.ns_pad + row] = lo;
+    }
+  } else if (o.qh) {
     if (which == 0) o.qh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
     else if (which == 1) o.kh[(seq * o.ns_pad + row) * o.hd + e] = __float2bfloat16_rn(v);
     else o.vth[(seq * o.hd + e) * o.ns_pad + row] = __float2bfloat16_rn(v);
