@@ -115,6 +115,7 @@ struct nvrec_model {
   float* blob = nullptr;        // all packed fp32 weights
   size_t blob_floats = 0;
   __half* blob_bf16 = nullptr;          // tensor-core operand packs (fast path, fp16)
+  __half* blob_x3 = nullptr;            // split-fp16 [hi | lo] packs (precise path)
   nvrec::ModelW W{};
   bool loaded = false;
 };
@@ -174,6 +175,16 @@ struct WorkspaceLayout {
 // Attention variant of a forward: 0 = fp32 SIMT (shapes outside the tensor-
 // core envelope), 1 = bf16 tensor cores (fast), 2 = split-bf16 tensor cores
 // (precise: hi*hi + hi*lo + lo*hi, fp32-class products).
+// NVREC_PRECISE_SIMT=1: the precise path's embedding and block tails on the
+// fp32 CUDA-core kernels (A/B of the split-operand tensor-core kernels)
+bool precise_simt() {
+  static const bool on = [] {
+    const char* e = getenv("NVREC_PRECISE_SIMT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int attn_mode(const Dims& D, int precision) {
   if (!nvrec::tc_supported(D)) return 0;
   return precision == NVREC_PREC_FAST ? 1 : 2;
@@ -271,13 +282,17 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
     // block li's spatial attention: Q/K/V were written by the previous stage
     cudaError_t e;
     int splits = 1;
+    // tensor-core tail of a non-last block: token_tc (fast) / token_x3 (precise)
+    const bool tc_tail = !last && nvrec::token_tc_supported(D) &&
+                         (fast ? m->W.tc.blk[li] != nullptr
+                               : (am == 2 && m->W.tc.blk3[li] != nullptr && !precise_simt()));
     if (am) {
       ProfScope ps(NVREC_STAGE_ATTN_TC, s);
       int nk = 1;
-      // the SIMT token kernel (last block) merges key-split partials itself
-      const bool defer = !fast || last || !nvrec::token_tc_supported(D) || !m->W.tc.blk[li];
+      // the SIMT token kernel merges key-split partials itself
+      const bool defer = !tc_tail;
       e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits,
-                                !defer,    // token_tc reads ao as fp16
+                                fast && tc_tail,   // token_tc reads ao as fp16
                                 am == 2);
       ps.kernels(nk);
     } else {
@@ -310,7 +325,26 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
     ta.out_slot = ip.frame_index ? ip.frame_index + (D.F - 1) : nullptr;
     ta.slot_stride = D.F;
     ta.frame_bytes = size_t(h) * w * D.c;
-    if (fast && !last && nvrec::token_tc_supported(D) && m->W.tc.blk[li]) {
+    if (tc_tail && am == 2) {
+      const nvrec::BlockW& bw = m->W.blk[li];
+      const nvrec::BlockW& bn = m->W.blk[li + 1];
+      nvrec::TokenX3Args tt{};
+      tt.b = b; tt.ns = A.ns; tt.ns_pad = A.ns_pad; tt.nt = D.nt;
+      tt.x = A.x; tt.ao = A.ao;
+      tt.w_blk = m->W.tc.blk3[li];
+      tt.w_next = m->W.tc.blk3[li + 1];
+      for (int j = 0; j < 5; ++j) tt.sc[j] = m->W.tc.sc_blk[li][j];
+      tt.sc[5] = m->W.tc.sc_blk[li + 1][5];
+      tt.b_proj_s = bw.proj_s_b; tt.ln_t_w = bw.ln_t_w; tt.ln_t_b = bw.ln_t_b;
+      tt.b_qkv_t = bw.qkv_t_b; tt.b_proj_t = bw.proj_t_b; tt.ln_m_w = bw.ln_m_w;
+      tt.ln_m_b = bw.ln_m_b; tt.b_fc1 = bw.fc1_b; tt.b_fc2 = bw.fc2_b;
+      tt.ln_s_next_w = bn.ln_s_w; tt.ln_s_next_b = bn.ln_s_b; tt.b_qkv_next = bn.qkv_s_b;
+      tt.qh = A.qh; tt.kh = A.kh; tt.vth = A.vth;
+      tt.qrank = ta.dst.rank;
+      ProfScope ps(NVREC_STAGE_TOKEN, s);
+      ps.kernels(3);
+      e = nvrec::launch_token_x3(tt, s);
+    } else if (tc_tail) {
       const nvrec::BlockW& bw = m->W.blk[li];
       const nvrec::BlockW& bn = m->W.blk[li + 1];
       nvrec::TokenTcArgs tt{};
@@ -359,6 +393,7 @@ int nvrec_model_destroy(nvrec_model* m) {
   if (!m) return 0;
   if (m->blob) cudaFree(m->blob);
   if (m->blob_bf16) cudaFree(m->blob_bf16);
+  if (m->blob_x3) cudaFree(m->blob_x3);
   delete m;
   return 0;
 }
@@ -506,6 +541,80 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     m->W.tc.emb_stage_elems = d * kst;
     m->W.tc.qkv0 = m->blob_bf16 + qoff;
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk[i] = m->blob_bf16 + blk_pack[i];
+
+    // ---- split-fp16 [hi | lo] packs for the precise path ----------------------
+    // W * 2^s with max|W| 2^s in [2^13, 2^14): hi = fp16(W 2^s) and lo =
+    // fp16(W 2^s - hi) keep 22 significant bits and lo stays normal; the
+    // kernels multiply their accumulators by 2^-s (TcW::sc_*).
+    if (m->blob_x3) { cudaFree(m->blob_x3); m->blob_x3 = nullptr; }
+    std::vector<__half> h3;
+    auto exponent_for = [](float mx) {
+      if (!(mx > 0.f) || !std::isfinite(mx)) return 0;
+      const int s = int(std::floor(std::log2(16384.0 / double(mx))));
+      return s < -60 ? -60 : (s > 60 ? 60 : s);
+    };
+    auto pack2 = [&](int N, int K, auto at, int sexp) {
+      const size_t base = h3.size();
+      h3.resize(base + 2 * size_t(N) * K);
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < K; ++k) {
+          const size_t idx = (size_t(k / 8) * (N / 8) + n / 8) * 64 + (n % 8) * 8 + k % 8;
+          const float v = std::ldexp(at(n, k), sexp);
+          const __half hi = __float2half_rn(v);
+          h3[base + idx] = hi;
+          h3[base + size_t(N) * K + idx] = __float2half_rn(v - __half2float(hi));
+        }
+      return base;
+    };
+    auto maxabs = [](int N, int K, auto at) {
+      float mx = 0.f;
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < K; ++k) mx = std::fmax(mx, std::fabs(at(n, k)));
+      return mx;
+    };
+    // embedding: one exponent for the whole image part of the weight
+    float emx = 0.f;
+    for (int o = 0; o < d; ++o)
+      for (int ci = 0; ci < c; ++ci)
+        for (int tt = 0; tt < T; ++tt)
+          for (int py = 0; py < p; ++py)
+            for (int px = 0; px < p; ++px) emx = std::fmax(emx, std::fabs(ew_at(o, ci, tt, py, px)));
+    const int se = exponent_for(emx);
+    m->W.tc.sc_emb = std::ldexp(1.f, -se);
+    const int kpy3 = c == 3 ? 2 : 4, kst3 = 16 * kpy3 * c;   // embed_tc's K stage (EmbSmem::kPy)
+    size_t emb3_off = 0;
+    for (int st = 0; st < T * 16 / kpy3; ++st) {
+      const int tt = st / (16 / kpy3), py0 = kpy3 * (st % (16 / kpy3));
+      const size_t o = pack2(d, kst3, [&](int n, int k) {
+        const int pyl = k / (16 * c), rem = k % (16 * c), px = rem / c, ci = rem % c;
+        return ew_at(n, ci, tt, py0 + pyl, px);
+      }, se);
+      if (st == 0) emb3_off = o;
+    }
+    auto lin3 = [&](const float* wt, int N, int K, float* sc) {
+      auto at = [&](int n, int k) { return wt[size_t(n) * K + k]; };
+      const int sx = exponent_for(maxabs(N, K, at));
+      *sc = std::ldexp(1.f, -sx);
+      return pack2(N, K, at, sx);
+    };
+    const size_t q3off = lin3(t[3 + 2], 3 * d, d, &m->W.tc.sc_qkv0);
+    std::vector<size_t> blk3;
+    for (int i = 0; i < D.layers; ++i) {
+      const float* const* bt = t + 3 + 18 * i;
+      float* sc = m->W.tc.sc_blk[i];
+      blk3.push_back(lin3(bt[4], d, d, sc + 0));          // attn_s.proj
+      lin3(bt[8], 3 * d, d, sc + 1);                      // attn_t.qkv
+      lin3(bt[10], d, d, sc + 2);                         // attn_t.proj
+      lin3(bt[14], 4 * d, d, sc + 3);                     // mlp.0
+      lin3(bt[16], d, 4 * d, sc + 4);                     // mlp.2
+      lin3(bt[2], 3 * d, d, sc + 5);                      // attn_s.qkv
+    }
+    CK(cudaMalloc(&m->blob_x3, h3.size() * sizeof(__half)), "cudaMalloc(x3)");
+    CK(cudaMemcpy(m->blob_x3, h3.data(), h3.size() * sizeof(__half), cudaMemcpyHostToDevice),
+       "cudaMemcpy(x3)");
+    m->W.tc.emb3 = m->blob_x3 + emb3_off;
+    m->W.tc.qkv0_3 = m->blob_x3 + q3off;
+    for (int i = 0; i < D.layers; ++i) m->W.tc.blk3[i] = m->blob_x3 + blk3[i];
   }
   m->loaded = true;
   return 0;
@@ -641,8 +750,9 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     e = nvrec::launch_masklist(mask_bits, b, nbytes, A.ns, A.list, A.rank, A.count, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "masklist launch");
-  if (fast && nvrec::embed_tc_supported(m->D)) {
+  if (am && nvrec::embed_tc_supported(m->D) && (am == 1 || !precise_simt())) {
     nvrec::EmbedTcArgs ea{};
+    ea.x3 = am == 2;
     ea.D = m->D;
     ea.tcw = &m->W.tc;
     ea.emb_wmsum = m->W.emb_wmsum; ea.emb_b = m->W.emb_b; ea.time_pos = m->W.time_pos;
@@ -654,7 +764,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     ea.x = A.x; ea.qh = A.qh; ea.kh = A.kh; ea.vth = A.vth;
     // the embedding output goes to block 0's tensor-core tail in fp16 (half
     // the traffic of that one hand-off; the tail keeps the residual in fp32)
-    A.x_half = A.xh && m->D.layers > 1 && nvrec::token_tc_supported(m->D) && m->W.tc.blk[0];
+    A.x_half = fast && A.xh && m->D.layers > 1 && nvrec::token_tc_supported(m->D) && m->W.tc.blk[0];
     ea.xh = A.x_half ? A.xh : nullptr;
     ea.b = b; ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns; ea.ns_pad = A.ns_pad;
     cudaError_t e2;

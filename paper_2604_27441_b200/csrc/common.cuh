@@ -108,6 +108,15 @@ struct TcW {
   // per block, contiguous: proj_s [64x64] | qkv_t [192x64] | proj_t [64x64] |
   // fc1 [256x64] | fc2 [64x256] | qkv_s [192x64]
   const __half* blk[8];
+  // Precise path (split fp16): every matrix W is packed as [hi | lo] blocks of
+  // W * 2^s (hi = fp16(W 2^s), lo = fp16(W 2^s - hi); s per matrix puts
+  // max|W| 2^s near 2^14 so lo stays a normal number); sc = 2^-s undoes it in
+  // the epilogue.  Same element order as the fast packs.
+  const __half* emb3;           // [T*16/kPy stages][hi 64 x 16 kPy c | lo ...], kPy = 2 (RGB) / 4
+  const __half* qkv0_3;         // [hi 192x64 | lo 192x64] block-0 qkv_s
+  const __half* blk3[8];        // per block: proj_s | qkv_t | proj_t | fc1 | fc2 | qkv_s, each [hi | lo]
+  float sc_emb, sc_qkv0;
+  float sc_blk[8][6];
 };
 
 struct ModelW {

@@ -20,6 +20,13 @@
 //              q/k/v + bias -> bf16 attention operands (Q, K rows; V^T).
 // GEMM per token: K = 512c (c = 3: 1536), N = 64; the u8 planes are read
 // once from HBM by TMA.
+//
+// X3 (precise path): fp32-class products.  Pixels are exact in fp16, so the
+// embedding is pix . W_hi + pix . W_lo (two MMAs per K step against the
+// [hi | lo] weight packs, TcW::emb3, scaled by 2^s); the LN output is split
+// y = y_hi + y_lo and the qkv GEMM is y_hi W_hi + y_hi W_lo + y_lo W_hi.  x
+// leaves in fp32; q/k/v leave as bf16 hi/lo pairs in the split attention
+// layouts (QkvDst::x3).  One CTA per SM (the doubled rings take ~135 KB).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -42,16 +49,19 @@ constexpr int kThreads = 192;
 // is done.  A K stage is kPy patch rows of one tubelet frame: 2 for RGB
 // (K = 96), 4 for depth (K = 64) so a depth stage is not dominated by its
 // barrier round trip.
-template <int C>
+template <int C, bool X3 = false>
 struct __align__(128) EmbSmem {
+  static constexpr int kX = X3 ? 2 : 1;                      // hi (+ lo) operand copies
   static constexpr int kPy = C == 3 ? 2 : 4;                 // patch rows per K stage
   static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame
   static constexpr int kNst = C == 3 ? 2 : 3;                // A/W (MMA operand) ring
   static constexpr int kNu8 = C == 3 ? 3 : 4;                // raw-pixel TMA ring
   static constexpr uint32_t kU8 = kTh * kPy * kTw * 16 * C; // raw pixels per stage
   static constexpr uint32_t kA = kRows * 16 * kPy * C * 2;  // fp16 A per stage
-  static constexpr uint32_t kW = 64 * 16 * kPy * C * 2;     // fp16 W per stage
-  static constexpr uint32_t kQkvW = 192 * 64 * 2, kA2 = kRows * 64 * 2;
+  static constexpr uint32_t kW1 = 64 * 16 * kPy * C * 2;    // fp16 W per stage (one copy)
+  static constexpr uint32_t kW = kW1 * kX;                  // [hi | lo]
+  static constexpr uint32_t kQkvW1 = 192 * 64 * 2, kA21 = kRows * 64 * 2;
+  static constexpr uint32_t kQkvW = kQkvW1 * kX, kA2 = kA21 * kX;
   static constexpr uint32_t kARegion = kNst * kA > kQkvW ? kNst * kA : kQkvW;
   static constexpr uint32_t kURegion = kNu8 * kU8 > kA2 ? kNu8 * kU8 : kA2;
   uint8_t a_raw[kARegion];        // A ring, then: qkv weights [192 x 64] fp16
@@ -78,12 +88,19 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int C>
+// bf16 hi/lo split of a pair: hi = bf16(p), lo = bf16(p - hi)
+__device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16(x, y);
+  const float2 h = unpack_bf16(hi);
+  lo = pack_bf16(x - h.x, y - h.y);
+}
+
+template <int C, bool X3>
 __global__ void __launch_bounds__(kThreads, 1)
 embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tcw) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using S = EmbSmem<C>;
+  using S = EmbSmem<C, X3>;
   // pointer arithmetic (not integer casts) keeps the shared address space
   S& sm = *reinterpret_cast<S*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -142,14 +159,16 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         const int ps = st % S::kNst;
         mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);
         mbar_expect_tx(&sm.w_full[ps], S::kW);
-        // the host packs 2-row stages back to back, so kPy/2 of them are one block
-        bulk_load(sm.w[ps], tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems, S::kW,
-                  &sm.w_full[ps]);
+        // the host packs 2-row stages back to back, so kPy/2 of them are one
+        // block (X3: one [hi | lo] pair per kernel stage)
+        const __half* src = X3 ? tcw.emb3 + size_t(st) * (S::kW / 2)
+                               : tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems;
+        bulk_load(sm.w[ps], src, S::kW, &sm.w_full[ps]);
       }
       // qkv weights into the A ring once the last embed MMA has read it
       mbar_wait(&sm.acc_full, 0);
-      mbar_expect_tx(&sm.wq_full, 192 * 64 * 2);
-      bulk_load(sm.a(0), tcw.qkv0, 192 * 64 * 2, &sm.wq_full);
+      mbar_expect_tx(&sm.wq_full, S::kQkvW);
+      bulk_load(sm.a(0), X3 ? tcw.qkv0_3 : tcw.qkv0, S::kQkvW, &sm.wq_full);
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA
@@ -162,9 +181,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         tc_fence_after();
         const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w[ps]);
 #pragma unroll
-        for (int kk = 0; kk < S::kPy * C; ++kk)
-          mma_ss(tmem, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
-                 sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
+        for (int kk = 0; kk < S::kPy * C; ++kk) {
+          const uint64_t ad = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
+          mma_ss(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
+          if (X3)   // pixels are exact: pix . W_lo completes the product
+            mma_ss(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+        }
         mma_commit(&sm.empty[ps]);
       }
       mma_commit(&sm.acc_full);
@@ -172,10 +194,19 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       mbar_wait(&sm.a2_ready, 0);
       tc_fence_after();
       const uint32_t idesc2 = idesc_f16(128, 192);
+      const uint32_t a2b = smem_u32(sm.u8(0)), wqb = smem_u32(sm.a(0));
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_ss(tmem + 64, sdesc(smem_u32(sm.u8(0)) + kk * 4096, 128, kSwizzleNone, 2048),
-               sdesc(smem_u32(sm.a(0)) + kk * 6144, 128, kSwizzleNone, 3072), idesc2, kk != 0);
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t yh = sdesc(a2b + kk * 4096, 128, kSwizzleNone, 2048);
+        const uint64_t wh = sdesc(wqb + kk * 6144, 128, kSwizzleNone, 3072);
+        mma_ss(tmem + 64, yh, wh, idesc2, kk != 0);
+        if (X3) {   // y_hi W_lo + y_lo W_hi
+          mma_ss(tmem + 64, yh, sdesc(wqb + S::kQkvW1 + kk * 6144, 128, kSwizzleNone, 3072),
+                 idesc2, 1);
+          mma_ss(tmem + 64, sdesc(a2b + S::kA21 + kk * 4096, 128, kSwizzleNone, 2048), wh,
+                 idesc2, 1);
+        }
+      }
       mma_commit(&sm.qkv_full);
     }
   } else {
@@ -230,14 +261,15 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       }
     }
     const bool mterm = last_slice && masked;
-    const float inv255 = 1.f / 255.f;
+    // (X3: the weights were scaled by 2^s; 2^-s / 255 is exactly 2^-s fl(1/255))
+    const float inv255 = X3 ? tcw.sc_emb * (1.f / 255.f) : 1.f / 255.f;
 #pragma unroll
     for (int o = 0; o < 64; ++o) {
       float v = fmaf(x[o], inv255, sm.par[o]);
       if (mterm) v += sm.par[128 + o];
       x[o] = v + sm.par[64 + o];
     }
-    if (valid && a.xh) {
+    if (valid && a.xh && !X3) {
       uint4* xo = reinterpret_cast<uint4*>(a.xh + (size_t(b * a.D.nt + it) * a.ns + s) * 64);
 #pragma unroll
       for (int o = 0; o < 64; o += 8)
@@ -266,9 +298,19 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         const int o = ki * 8 + j;
         y[j] = (x[o] - mean) * rstd * sm.par[192 + o] + sm.par[256 + o];
       }
-      *reinterpret_cast<uint4*>(a2row + ki * 2048) =
-          make_uint4(pack_h2(y[0], y[1]), pack_h2(y[2], y[3]), pack_h2(y[4], y[5]),
-                     pack_h2(y[6], y[7]));
+      uint32_t hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hi[j] = pack_h2(y[2 * j], y[2 * j + 1]);
+      *reinterpret_cast<uint4*>(a2row + ki * 2048) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      if (X3) {
+        uint32_t lo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&hi[j]));
+          lo[j] = pack_h2(y[2 * j] - h.x, y[2 * j + 1] - h.y);
+        }
+        *reinterpret_cast<uint4*>(a2row + S::kA21 + ki * 2048) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
     }
     fence_proxy_async();
     mbar_arrive(&sm.a2_ready);
@@ -286,8 +328,34 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       const int which = c6 >> 1, head = c6 & 1;
       const size_t seq = size_t(b * a.D.nt + it) * 2 + head;
       float v[32];
+      const float qs = X3 ? tcw.sc_qkv0 : 1.f;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + sm.par[320 + 32 * c6 + e];
+      for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(r[e]), qs, sm.par[320 + 32 * c6 + e]);
+      if (X3) {
+        // bf16 hi/lo pairs: Q/K rows [hi 32 | lo 32], V^T rows e (hi), 32 + e (lo)
+        if (which < 2) {
+          if (which == 0 && qrow < 0) continue;
+          uint4* d4 = reinterpret_cast<uint4*>((which == 0 ? a.qh : a.kh) +
+                                               (seq * a.ns_pad + (which == 0 ? qrow : s)) * 64);
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) split_bf16(v[e + 2 * j], v[e + 2 * j + 1], h[j], l[j]);
+            d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+            d4[4 + e / 8] = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+        } else {
+          __nv_bfloat16* dst = a.vth + seq * 64 * a.ns_pad + s;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const __nv_bfloat16 h = __float2bfloat16_rn(v[e]);
+            dst[size_t(e) * a.ns_pad] = h;
+            dst[size_t(32 + e) * a.ns_pad] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
+          }
+        }
+        continue;
+      }
       if (which < 2) {
         if (which == 0 && qrow < 0) continue;
         __nv_bfloat16* dst = (which == 0 ? a.qh : a.kh) +
@@ -323,7 +391,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int C>
+template <int C, bool X3>
 cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
   auto fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
@@ -339,10 +407,10 @@ cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const size_t smem = sizeof(EmbSmem<C>) + 128;
-  if (cudaError_t e = smem_optin(embed_tc_kernel<C>, int(smem))) return e;
+  const size_t smem = sizeof(EmbSmem<C, X3>) + 128;
+  if (cudaError_t e = smem_optin(embed_tc_kernel<C, X3>, int(smem))) return e;
   const int tiles = ((a.nh + kTh - 1) / kTh) * ((a.nw + kTw - 1) / kTw);
-  launch_seq(embed_tc_kernel<C>, dim3(tiles, a.D.nt, a.b), kThreads, smem, s, tm, a, *a.tcw);
+  launch_seq(embed_tc_kernel<C, X3>, dim3(tiles, a.D.nt, a.b), kThreads, smem, s, tm, a, *a.tcw);
   return cudaGetLastError();
 }
 
@@ -353,7 +421,8 @@ bool embed_tc_supported(const Dims& D) {
 }
 
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s) {
-  return a.D.c == 3 ? launch_c<3>(a, s) : launch_c<1>(a, s);
+  if (a.x3) return a.D.c == 3 ? launch_c<3, true>(a, s) : launch_c<1, true>(a, s);
+  return a.D.c == 3 ? launch_c<3, false>(a, s) : launch_c<1, false>(a, s);
 }
 
 }  // namespace nvrec

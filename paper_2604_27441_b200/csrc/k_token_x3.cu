@@ -1,0 +1,406 @@
+// k_token_x3.cu -- the fused block tail of a NON-LAST block on the PRECISE
+// path (model.py:60-64, then the next block's :59/:37), on tcgen05 with
+// fp32-class products: every GEMM operand is split a = a_hi + a_lo (fp16,
+// weights pre-scaled by 2^s so their lo parts stay normal, TcW::blk3) and
+// D = A_hi W_hi + A_hi W_lo + A_lo W_hi, fp32 accumulation; LayerNorm,
+// softmax, GELU and the residual stay fp32.
+//
+// The split weights of one block tail (256 KB) do not fit in shared memory
+// together, so the tail runs as three persistent phase kernels, each with its
+// phase's weights resident and the fp32 residual x handed over in HBM:
+//   phase 0   x += proj_s(ao);  x += proj_t(attn_t(qkv_t(LN_t(x))))   80 KB
+//   phase 1   x += fc2(GELU(fc1(LN_m(x))))                             128 KB
+//   phase 2   q,k,v = qkv_s'(LN_s'(x)) -> split bf16 attention operands  48 KB
+// Tiles, slots and the per-warp position layout follow k_token_tc.cu (lane =
+// j*nt + slice, the temporal attention is warp shuffles).  fc1 -> fc2 runs in
+// two halves of 128 hidden units: fc1 half -> TMEM, GELU written back in place
+// as fp16 [hi 32 | lo 32] column groups, fc2 reads them as the A operand from
+// TMEM; the accumulator sits beside the half (192 of the slot's 256 columns).
+#include "launch.cuh"
+#include "sm100.cuh"
+
+namespace nvrec {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kSlots = 2;
+constexpr int kThreads = 128 * kSlots;
+// element offsets of the [hi | lo] packs inside one block's blk3 pack
+constexpr uint32_t kX3ProjS = 0, kX3QkvT = 8192, kX3ProjT = 32768, kX3Fc1 = 40960,
+                   kX3Fc2 = 73728, kX3QkvS = 106496, kX3Blk = 131072;
+// weights resident per phase (halves) and their offset inside the block pack
+__host__ __device__ constexpr uint32_t ph_elems(int ph) {
+  return ph == 0 ? kX3Fc1 : (ph == 1 ? kX3QkvS - kX3Fc1 : kX3Blk - kX3QkvS);
+}
+__host__ __device__ constexpr uint32_t ph_base(int ph) {
+  return ph == 0 ? 0u : (ph == 1 ? kX3Fc1 : kX3QkvS);
+}
+// staged parameter vectors (floats), as k_token_tc.cu
+constexpr int kPBProjS = 0, kPLnTw = 64, kPLnTb = 128, kPBQkvT = 192, kPBProjT = 384,
+              kPLnMw = 448, kPLnMb = 512, kPBFc1 = 576, kPBFc2 = 832, kPLnSw = 896,
+              kPLnSb = 960, kPBQkvN = 1024, kParFloats = 1216;
+constexpr uint32_t kABytes = 128 * 64 * 2;       // one fp16 [128 x 64] operand copy
+
+template <int PH>
+struct __align__(128) X3Smem {
+  __half w[ph_elems(PH)];
+  uint8_t a[kSlots][2 * kABytes];   // per slot: A_hi | A_lo
+  float par[kParFloats];
+  uint64_t bar_w, bar_d[kSlots];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// fp16 hi/lo split of a pair
+__device__ __forceinline__ void split_h2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  hi = pack_h2(x, y);
+  const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&hi));
+  lo = pack_h2(x - h.x, y - h.y);
+}
+// bf16 hi/lo split of a pair (the attention operands)
+__device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16(x, y);
+  const float2 h = unpack_bf16(hi);
+  lo = pack_bf16(x - h.x, y - h.y);
+}
+
+// row m of 64 fp32 -> [hi | lo] fp16 K-major core-matrix operands; cols
+// [c0, c0 + 8 nk) only (the temporal attention writes one head at a time)
+__device__ __forceinline__ void put_row_x3(uint8_t* base, int m, const float* y, int k0 = 0,
+                                           int nk = 8) {
+#pragma unroll
+  for (int ki = 0; ki < 8; ++ki) {
+    if (ki >= nk) break;
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) split_h2(y[8 * ki + 2 * j], y[8 * ki + 2 * j + 1], h[j], l[j]);
+    *reinterpret_cast<uint4*>(base + (k0 + ki) * 2048 + m * 16) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(base + kABytes + (k0 + ki) * 2048 + m * 16) =
+        make_uint4(l[0], l[1], l[2], l[3]);
+  }
+}
+
+__device__ __forceinline__ void layernorm64(const float* x, float* y, const float* g,
+                                            const float* bt) {
+  float mean = 0.f;
+#pragma unroll
+  for (int o = 0; o < 64; ++o) mean += x[o];
+  mean *= (1.f / 64.f);
+  float var = 0.f;
+#pragma unroll
+  for (int o = 0; o < 64; ++o) var = fmaf(x[o] - mean, x[o] - mean, var);
+  const float rstd = rsqrtf(var * (1.f / 64.f) + 1e-5f);
+#pragma unroll
+  for (int o = 0; o < 64; ++o) y[o] = (x[o] - mean) * rstd * g[o] + bt[o];
+}
+
+template <int PH>
+__global__ void __launch_bounds__(kThreads, 1)
+token_x3_kernel(TokenX3Args a) {
+  pdl_wait();
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  using S = X3Smem<PH>;
+  S& sm = *reinterpret_cast<S*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp >> 2, wq = warp & 3;        // tile slot, TMEM lane quarter
+  const int nt = a.nt;
+  const int ppw = 32 / nt;                          // whole positions per warp
+  const int P = 4 * ppw;                            // positions per tile
+  const int tiles_per_b = (a.ns + P - 1) / P;
+  const int n_tiles = tiles_per_b * a.b;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar_w, 1);
+    for (int k = 0; k < kSlots; ++k) mbar_init(&sm.bar_d[k], 1);
+    fence_mbar_init();
+    constexpr uint32_t bytes = ph_elems(PH) * 2;
+    mbar_expect_tx(&sm.bar_w, bytes);
+    const __half* src = (PH == 2 ? a.w_next : a.w_blk) + ph_base(PH);
+    // bulk copies of <= 64 KB each
+    for (uint32_t off = 0; off < bytes; off += 65536)
+      bulk_load(reinterpret_cast<uint8_t*>(sm.w) + off, reinterpret_cast<const uint8_t*>(src) + off,
+                bytes - off < 65536 ? bytes - off : 65536, &sm.bar_w);
+  }
+  {
+    const struct { const float* src; int off, n; } vecs[12] = {
+        {a.b_proj_s, kPBProjS, 64}, {a.ln_t_w, kPLnTw, 64}, {a.ln_t_b, kPLnTb, 64},
+        {a.b_qkv_t, kPBQkvT, 192}, {a.b_proj_t, kPBProjT, 64}, {a.ln_m_w, kPLnMw, 64},
+        {a.ln_m_b, kPLnMb, 64}, {a.b_fc1, kPBFc1, 256}, {a.b_fc2, kPBFc2, 64},
+        {a.ln_s_next_w, kPLnSw, 64}, {a.ln_s_next_b, kPLnSb, 64}, {a.b_qkv_next, kPBQkvN, 192}};
+#pragma unroll 1
+    for (int v = 0; v < 12; ++v)
+      for (int i = threadIdx.x; i < vecs[v].n; i += blockDim.x) sm.par[vecs[v].off + i] = vecs[v].src[i];
+  }
+  if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  mbar_wait(&sm.bar_w, 0);
+
+  const float* P_ = sm.par;
+  const int m = wq * 32 + lane;                     // row == TMEM lane
+  const uint32_t lane_off = uint32_t(wq * 32) << 16;
+  const uint32_t tbase = sm.tmem_base + 256 * slot; // this slot's 256 columns
+  const int jl = lane / nt, it = lane - jl * nt;    // position in warp, slice
+  const bool row_live = jl < ppw;
+  uint8_t* A = sm.a[slot];
+  const uint32_t ab = smem_u32(A);
+  const uint32_t wb = smem_u32(sm.w) - ph_base(PH) * 2;   // + element offset * 2 = a block pack matrix
+  const bool issuer = wq == 0 && lane == 0;
+  uint32_t pd = 0;
+  auto run = [&](auto issue) {
+    fence_proxy_async();
+    tc_fence_before();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+    if (issuer) {
+      tc_fence_after();
+      issue();
+      mma_commit(&sm.bar_d[slot]);
+    }
+    mbar_wait(&sm.bar_d[slot], pd & 1);
+    ++pd;
+    tc_fence_after();
+  };
+  // D[dcol..] (=) A(smem [hi|lo], K = 64) . W ([hi|lo] at element offset woff
+  // of the block pack, N x 64, rows n0.. of an Nfull-row matrix)
+  auto issue_a = [&](uint32_t dcol, uint32_t woff, int N, int Nfull, int n0) {
+    const uint32_t idesc = idesc_f16(128, N), lbo_b = (Nfull / 8) * 128;
+    const uint32_t bh = wb + woff * 2 + (n0 / 8) * 128, bl = bh + Nfull * 64 * 2;
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t ah = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
+      const uint64_t al = sdesc(ab + kABytes + kk * 4096, 128, kSwizzleNone, 2048);
+      const uint64_t wh = sdesc(bh + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
+      const uint64_t wl = sdesc(bl + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
+      mma_ss(tbase + dcol, ah, wh, idesc, kk != 0);
+      mma_ss(tbase + dcol, ah, wl, idesc, 1);
+      mma_ss(tbase + dcol, al, wh, idesc, 1);
+    }
+  };
+  auto gemm_a = [&](uint32_t dcol, uint32_t woff, int N) {
+    run([&] { issue_a(dcol, woff, N, N, 0); });
+  };
+  // x += D[64 cols at col] * sc + bias
+  auto add64 = [&](float* x, uint32_t col, float sc, const float* bias) {
+    uint32_t r[64];
+    tmem_ld32(tbase + lane_off + col, r);
+    tmem_ld32(tbase + lane_off + col + 32, r + 32);
+    tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 64; ++e) x[e] += fmaf(__uint_as_float(r[e]), sc, bias[e]);
+  };
+  const float scale = rsqrtf(32.f);
+
+  for (int tile = blockIdx.x * kSlots + slot; tile < n_tiles; tile += gridDim.x * kSlots) {
+    const int b = tile / tiles_per_b;
+    const int s = (tile - b * tiles_per_b) * P + wq * ppw + jl;
+    const bool valid = row_live && s < a.ns;
+    const size_t xrow = (size_t(b * nt + it) * a.ns + s) * 64;
+    float x[64], y[64];
+    {
+      const float4* xi = reinterpret_cast<const float4*>(a.x + xrow);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        float4 u = valid ? xi[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        x[4 * q] = u.x; x[4 * q + 1] = u.y; x[4 * q + 2] = u.z; x[4 * q + 3] = u.w;
+      }
+    }
+    if constexpr (PH == 0) {
+      // ---- x += proj_s(ao) ---------------------------------------------------
+      {
+        const float4* ai = reinterpret_cast<const float4*>(a.ao + xrow);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float4 u = valid ? ai[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          y[4 * q] = u.x; y[4 * q + 1] = u.y; y[4 * q + 2] = u.z; y[4 * q + 3] = u.w;
+        }
+      }
+      put_row_x3(A, m, y);
+      gemm_a(0, kX3ProjS, 64);
+      add64(x, 0, a.sc[0], P_ + kPBProjS);
+      // ---- qkv_t(LN_t(x)); temporal attention by warp shuffles ----------------
+      layernorm64(x, y, P_ + kPLnTw, P_ + kPLnTb);
+      put_row_x3(A, m, y);
+      gemm_a(0, kX3QkvT, 192);
+      const float sq = a.sc[1];
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        float q[32], kk_[32], vv[32];
+        tmem_ld32(tbase + lane_off + 32 * hh, reinterpret_cast<uint32_t*>(q));
+        tmem_ld32(tbase + lane_off + 64 + 32 * hh, reinterpret_cast<uint32_t*>(kk_));
+        tmem_ld32(tbase + lane_off + 128 + 32 * hh, reinterpret_cast<uint32_t*>(vv));
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          q[e] = fmaf(q[e], sq, P_[kPBQkvT + 32 * hh + e]);
+          kk_[e] = fmaf(kk_[e], sq, P_[kPBQkvT + 64 + 32 * hh + e]);
+          vv[e] = fmaf(vv[e], sq, P_[kPBQkvT + 128 + 32 * hh + e]);
+        }
+        float sc[8];
+        float mx = -INFINITY;
+        const int l0 = jl * nt;                        // lane of slice 0
+#pragma unroll
+        for (int ik = 0; ik < 8; ++ik) {
+          if (ik >= nt) break;
+          float acc = 0.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) acc = fmaf(q[e], __shfl_sync(0xffffffffu, kk_[e], l0 + ik), acc);
+          sc[ik] = acc * scale;
+          mx = fmaxf(mx, sc[ik]);
+        }
+        float den = 0.f;
+#pragma unroll
+        for (int ik = 0; ik < 8; ++ik) {
+          if (ik >= nt) break;
+          sc[ik] = expf(sc[ik] - mx);
+          den += sc[ik];
+        }
+        const float inv = 1.f / den;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) q[e] = 0.f;        // q -> output accumulator
+#pragma unroll
+        for (int ik = 0; ik < 8; ++ik) {
+          if (ik >= nt) break;
+          const float p = sc[ik] * inv;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) q[e] = fmaf(p, __shfl_sync(0xffffffffu, vv[e], l0 + ik), q[e]);
+        }
+        if (!row_live) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) q[e] = 0.f;
+        }
+        put_row_x3(A, m, q, 4 * hh, 4);                // head hh -> A columns [32hh, 32hh+32)
+      }
+      // ---- x += proj_t(o) ------------------------------------------------------
+      gemm_a(0, kX3ProjT, 64);
+      add64(x, 0, a.sc[2], P_ + kPBProjT);
+      if (valid) {
+        float4* xo = reinterpret_cast<float4*>(a.x + xrow);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+      }
+    } else if constexpr (PH == 1) {
+      // ---- x += fc2(GELU(fc1(LN_m(x)))) in two halves of 128 hidden units ------
+      layernorm64(x, y, P_ + kPLnMw, P_ + kPLnMb);
+      put_row_x3(A, m, y);
+      const float s1 = a.sc[3], s2 = a.sc[4];
+      // fc2 K step kk (16 hidden units of half H) from the TMEM column groups
+      auto issue_fc2 = [&](int H) {
+        const uint32_t idesc = idesc_f16(128, 64), lbo_b = 8 * 128;
+        const uint32_t bh = wb + kX3Fc2 * 2, bl = bh + 64 * 256 * 2;
+        for (int kk = 0; kk < 8; ++kk) {
+          const int kg = 8 * H + kk;                    // global K16 step
+          const uint32_t ah = tbase + (kk >> 2) * 64 + (kk & 3) * 8;
+          const uint64_t wh = sdesc(bh + kg * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
+          const uint64_t wl = sdesc(bl + kg * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
+          mma_ts(tbase + 128, ah, wh, idesc, kg != 0);
+          mma_ts(tbase + 128, ah, wl, idesc, 1);
+          mma_ts(tbase + 128, ah + 32, wh, idesc, 1);
+        }
+      };
+      // GELU of the fc1 half in TMEM cols [0,128) -> [hi 32 | lo 32] per 64
+#pragma unroll 1
+      for (int H = 0; H < 2; ++H) {
+        if (H == 0) run([&] { issue_a(0, kX3Fc1, 128, 256, 0); });
+        else run([&] { issue_fc2(0); issue_a(0, kX3Fc1, 128, 256, 128); });
+#pragma unroll 1
+        for (int g = 0; g < 2; ++g) {
+          uint32_t r[64], lo[32];
+          tmem_ld32(tbase + lane_off + 64 * g, r);
+          tmem_ld32(tbase + lane_off + 64 * g + 32, r + 32);
+          tmem_wait_ld();
+          const float* bias = P_ + kPBFc1 + 128 * H + 64 * g;
+#pragma unroll
+          for (int e = 0; e < 64; e += 2)
+            split_h2(gelu_erf(fmaf(__uint_as_float(r[e]), s1, bias[e])),
+                     gelu_erf(fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])), r[e / 2], lo[e / 2]);
+          tmem_st16(tbase + lane_off + 64 * g, r);
+          tmem_st16(tbase + lane_off + 64 * g + 16, r + 16);
+          tmem_st16(tbase + lane_off + 64 * g + 32, lo);
+          tmem_st16(tbase + lane_off + 64 * g + 48, lo + 16);
+        }
+        tmem_wait_st();
+      }
+      run([&] { issue_fc2(1); });
+      add64(x, 128, s2, P_ + kPBFc2);
+      if (valid) {
+        float4* xo = reinterpret_cast<float4*>(a.x + xrow);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+      }
+    } else {
+      // ---- next block's LN_s + qkv_s -> split bf16 attention operands ----------
+      layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
+      put_row_x3(A, m, y);
+      gemm_a(0, kX3QkvS, 192);
+      int qrow = s;
+      if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
+      const float sq = a.sc[5];
+#pragma unroll 1
+      for (int c6 = 0; c6 < 6; ++c6) {
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_off + 32 * c6, r);
+        tmem_wait_ld();
+        if (!valid) continue;
+        const int which = c6 >> 1, head = c6 & 1;
+        const size_t seq = size_t(b * nt + it) * 2 + head;
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(r[e]), sq, P_[kPBQkvN + 32 * c6 + e]);
+        if (which < 2) {
+          if (which == 0 && qrow < 0) continue;
+          uint4* d4 = reinterpret_cast<uint4*>((which == 0 ? a.qh : a.kh) +
+                                               (seq * a.ns_pad + (which == 0 ? qrow : s)) * 64);
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) split_bf16(v[e + 2 * j], v[e + 2 * j + 1], h[j], l[j]);
+            d4[e / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+            d4[4 + e / 8] = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+        } else {
+          __nv_bfloat16* dst = a.vth + seq * 64 * a.ns_pad + s;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const __nv_bfloat16 h = __float2bfloat16_rn(v[e]);
+            dst[size_t(e) * a.ns_pad] = h;
+            dst[size_t(32 + e) * a.ns_pad] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
+          }
+        }
+      }
+    }
+    // every thread's TMEM reads precede the next tile's first MMA (run()'s barrier)
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(sm.tmem_base);
+  pdl_trigger();
+}
+
+template <int PH>
+cudaError_t launch_phase(const TokenX3Args& a, cudaStream_t s) {
+  const size_t smem = sizeof(X3Smem<PH>) + 128;
+  if (cudaError_t e = smem_optin(token_x3_kernel<PH>, int(smem))) return e;
+  const int sms = sm_count();
+  const int P = 4 * (32 / a.nt);
+  const int tiles = ((a.ns + P - 1) / P) * a.b;
+  const int ctas = (tiles + kSlots - 1) / kSlots;
+  launch_seq(token_x3_kernel<PH>, ctas < sms ? ctas : sms, kThreads, smem, s, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_token_x3(const TokenX3Args& a, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = launch_phase<0>(a, s)) != cudaSuccess) return e;
+  if ((e = launch_phase<1>(a, s)) != cudaSuccess) return e;
+  return launch_phase<2>(a, s);
+}
+
+}  // namespace nvrec

@@ -82,6 +82,7 @@ struct EmbedTcArgs {
   __half* xh;                     // or: the embedding output in fp16 (token_tc input)
   __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
   int b, h, w, nh, nw, ns, ns_pad;
+  int x3;                         // precise: split operands (TcW emb3/qkv0_3), fp32 x
 };
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 
@@ -99,6 +100,21 @@ struct TokenTcArgs {
   const int* qrank;             // compact Q rows for a pruned next block, or null
 };
 cudaError_t launch_token_tc(const TokenTcArgs& a, cudaStream_t s);
+
+// precise (split-fp16) tensor-core tail of a non-last block (k_token_x3.cu):
+// three phase kernels, same envelope as token_tc
+struct TokenX3Args {
+  int b, ns, ns_pad, nt;
+  float* x; const float* ao;    // fp32 residual (in/out) and attention output
+  const __half* w_blk;          // this block's [hi | lo] pack (TcW::blk3)
+  const __half* w_next;         // next block's pack (its qkv_s)
+  float sc[6];                  // 2^-s: proj_s, qkv_t, proj_t, fc1, fc2, next qkv_s
+  const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
+  const float *b_fc1, *b_fc2, *ln_s_next_w, *ln_s_next_b, *b_qkv_next;
+  __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;   // split layouts (QkvDst::x3)
+  const int* qrank;             // compact Q rows for a pruned next block, or null
+};
+cudaError_t launch_token_x3(const TokenX3Args& a, cudaStream_t s);
 
 cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s);
 cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s);

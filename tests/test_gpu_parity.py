@@ -255,7 +255,9 @@ def test_fast_vs_reference_error_budget_720p():
 def _attn_mode_run(mode, path, precision="fast"):
     import subprocess
     import sys
-    env = dict(os.environ, NVREC_ATTN_MODE=mode)
+    # one key split: every work item walks several key tiles, so the
+    # speculative max (and its overflow fix-up) is exercised
+    env = dict(os.environ, NVREC_ATTN_MODE=mode, NVREC_ATTN_SPLITS="1")
     here = os.path.dirname(os.path.abspath(__file__))
     subprocess.run([sys.executable, os.path.join(here, "attn_mode_probe.py"), path, precision],
                    check=True, env=env, timeout=300)
