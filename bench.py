@@ -1,6 +1,6 @@
 """Benchmark: recovered 1280x720 RGB-D frames/s per GPU (+ p50 latency).
 
-Workload (BASELINE.json configs[2] x configs[4]): each GPU serves S
+Headline workload (BASELINE.json configs[2] x configs[4]): each GPU serves S
 independent 720p RGB-D conference streams (default 8, so 8 GPUs = the
 64-stream multi-party config; weak scaling, no collective on the data
 path).  One step = one frame of every stream, both modalities:
@@ -13,15 +13,30 @@ path).  One step = one frame of every stream, both modalities:
               depth on two CUDA streams): u8 stack of 5 references + the
               corrupted plane, model forward, quantise, masked merge.
 
+Arithmetic: ``--precision precise`` (the default and the headline) is
+fp32-class -- every tensor-core product from split operands (a = hi + lo,
+hi*hi + hi*lo + lo*hi, fp32 accumulation; 720p max-abs ~5e-7 against the
+reference's fp32 forward); the ``fast`` path (bf16/fp16 operands) is
+measured beside it.
+
 ``value`` = frames/s with inputs resident in HBM (device-timed, CUDA
-events, max over ranks).  ``e2e`` = the same step through host buffers:
-pinned H2D of every stream's loss-mask job and its 6 planes per modality
-(exactly what the reference recovery request carries, recovery.py:219-227)
-and D2H of the recovered planes, inside the timed region.
+events, max over ranks).  ``e2e`` = the same step through host buffers
+(RecoveryPipeline): pinned H2D of every stream's new corrupted plane and
+loss-mask job, recovery on the device-resident reference rings, D2H of the
+recovered planes, inside the timed region.  ``configs`` holds the other
+BASELINE.json shapes and mask densities (320x240, 640x480, 720p at 10% and
+20% block loss, 1920x1088 at 20%, 64 streams on one GPU).
 
 ``--impl reference`` times the reference CPU path (the oracle restatement
-of RecoveryServer._recover in fp32 torch-CPU ops -- the same ATen kernels
-the reference module calls) on the host cores, rank 0 only.
+of the receiver's loss mask and RecoveryServer._recover in fp32 torch-CPU
+ops -- the same ATen kernels the reference module calls) on the host cores,
+rank 0 only, on the SAME synthetic inputs as the GPU arm: the same streams'
+planes, the same GE-dropped shards, the same random-init weights; each step
+is one stream's RGB-D frame (a bounded sample of the 8-stream step).
+
+``--gpus N`` without torchrun re-launches itself under torch.distributed.run
+with N ranks (127.0.0.1).  ``--dry-run`` exercises only the launch / timing
+/ reporting logic (gloo, no GPU work; used by the CPU tests).
 """
 
 from __future__ import annotations
@@ -29,10 +44,11 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
+import threading
 import time
 
 import numpy as np
@@ -45,6 +61,15 @@ H, W = 720, 1280
 METRIC = "recovered RGB-D frames/sec/GPU and p50 per-frame latency at 720p"
 MODS = (("rgb", 3, 1024), ("depth", 1, 512))      # name, channels, shard L
 MUFU_PEAK = 148 * 16 * 1.965e9                      # ex2/s, derived
+PRECISE_DTYPE = "f32"
+PRECISE_NOTE = ("fp32-class: every tensor-core product from split operands (bf16 hi/lo for "
+                "attention Q/K/V/P, fp16 hi/lo with per-matrix 2^s pre-scale for the weights "
+                "and activations of the embed/linear GEMMs), hi*hi + hi*lo + lo*hi with fp32 "
+                "accumulation; softmax, LayerNorm, GELU, residual, head fp32; measured 720p "
+                "max-abs 4.8e-7 (RGB) / 5.7e-7 (depth) vs the reference's fp32 forward")
+WORKLOAD_720P = ("1280x720 RGB-D streams (configs[2] x configs[4]): %d streams/GPU, GE loss "
+                 "(p_gb=0.0155,p_bg=0.5) on body shards of synthetic P-frame headers (~10%% "
+                 "changed blocks), k=5 refs, random-init weights (seed 0)")
 
 
 def parse():
@@ -54,10 +79,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams-per-gpu", type=int, default=8)
-    ap.add_argument("--precision", default="fast", choices=["fast", "precise"])
+    ap.add_argument("--precision", default="precise", choices=["fast", "precise"])
     ap.add_argument("--latency-iters", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the fast-path, other-config and density lines")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch/timing/report logic only (gloo, no GPU work)")
     return ap.parse_args()
 
 
@@ -68,129 +97,225 @@ def dist_env():
     return rank, world, local
 
 
+def spawn_ranks(args) -> None:
+    """``--gpus N`` outside torchrun: re-run this script with N ranks."""
+    if args.gpus <= 1 or "RANK" in os.environ:
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def max_over_ranks(ms: float, dist_on: bool, device=None) -> float:
+    if not dist_on:
+        return ms
+    t = torch.tensor([ms], device=device) if device is not None else torch.tensor([ms])
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ----------------------------------------------------------------------------
-# clocks (nvidia-smi sampled during the timed region)
+# clocks sampled DURING the timed region (NVML thread, 2 ms period)
 
 class ClockSampler:
-    def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q,
-                                       "--format=csv,noheader,nounits", "-lms", "20"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
-        except OSError:
-            self.p = None
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
-    def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.seek(0)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.sm, self.reasons, self.mx = [], set(), None
+        self.stop_ev = threading.Event()
+        self.err = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001 -- report, do not fail the bench
+            self.nv, self.err = None, repr(e)
+        self.period = period_s
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        os.unlink(self.f.name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
+                return
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop_ev.set()
+        if self.nv is not None:
+            self.th.join()
+        return False
+
+    def result(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: %s" % self.err]}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "NVML every 2 ms during the timed device region"}
 
 
 # ----------------------------------------------------------------------------
-# synthetic per-rank workload
+# synthetic inputs, shared by the GPU arm and the reference (CPU) arm
+
+def stream_planes(c: int, h: int, w: int, sid: int, F: int = 6) -> np.ndarray:
+    """(F, h, w, c) u8: a random 8x8-block texture drifting one pixel per
+    frame (5 references + the corrupted plane of stream ``sid``)."""
+    rng = np.random.default_rng(1000 * c + 7919 * sid)
+    base = rng.integers(0, 256, (h // 8 + 2, w // 8 + 2, c), dtype=np.uint8)
+    tex = np.kron(base, np.ones((8, 8, 1), np.uint8))
+    return np.stack([tex[i % 8: i % 8 + h, 0:w] for i in range(F)])
+
+
+class Workload:
+    """One BASELINE config: resolution, streams, and how a stream's loss mask
+    arises -- ``("ge",)`` Gilbert-Elliott body-shard loss, ``("bern", p)``
+    Bernoulli shard loss (both through the receiver/codec mask), or
+    ``("block", r)`` a synthetic block mask (nvrec data.synthetic_mask)."""
+
+    def __init__(self, name, h, w, stream_ids, loss=("ge",)):
+        self.name, self.h, self.w, self.loss = name, h, w, loss
+        self.ids = list(stream_ids)
+
+    def planes(self, c, sid):
+        return stream_planes(c, self.h, self.w, sid)
+
+    def job(self, c, L, s, sid):
+        """(header, n_data, received, encoded_len) for mask kinds ge/bern."""
+        from tools.synth import GilbertElliott, p_frame_shards
+        rng = np.random.default_rng(sid + c)
+        if self.loss[0] == "ge":
+            drop = GilbertElliott(seed=sid + 17 * c).drop
+        else:
+            lrng = np.random.default_rng(50000 + sid + 17 * c)
+            drop = (lambda: bool(lrng.random() < self.loss[1]))
+        hdr, nd, recv, enc = p_frame_shards(rng, self.w, self.h, c, L, drop, present_ratio=0.1)
+        if recv.all():                     # every stream needs recovery
+            recv[1 + (s % max(1, nd - 1))] = False
+        return hdr, nd, recv, enc
+
+    def grid(self, c, sid):
+        """Block grid for mask kind ``block``."""
+        from paper_2604_27441_b200.data import synthetic_mask
+        rng = np.random.default_rng(90000 + sid + 17 * c)
+        m = synthetic_mask(self.h, self.w, self.loss[1], rng)
+        g = m[::16, ::16].copy()
+        if not g.any():
+            g[0, 0] = True
+        return g
+
+    def describe(self):
+        if self.loss[0] == "ge":
+            kind = "GE loss (p_gb=0.0155,p_bg=0.5) on body shards"
+        elif self.loss[0] == "bern":
+            kind = "Bernoulli %.0f%% body-shard loss" % (100 * self.loss[1])
+        else:
+            kind = "%.0f%% synthetic block mask (data.synthetic_mask)" % (100 * self.loss[1])
+        return "%dx%d RGB-D, %d streams, %s" % (self.w, self.h, len(self.ids), kind)
+
 
 class ModalityWork:
-    """S streams of one modality: references + corrupted planes, loss-mask
-    jobs, device-resident and pinned-host copies."""
+    """The streams of one modality of a Workload on one GPU: device-resident
+    reference planes + corrupted planes, loss-mask jobs (or block masks),
+    pinned host copies, the engine, and (headline) the serving pipeline."""
 
-    def __init__(self, name, c, L, stream_ids, device, precision):
+    def __init__(self, wl: Workload, name, c, L, device, precision, pipeline=False, engine=None):
         from paper_2604_27441_b200 import Checkpoint, ModelConfig
         from paper_2604_27441_b200.lossmask import LossMaskBatch, PFrameShards
-        from paper_2604_27441_b200.recovery import RecoveryEngine, stack_slots
-        from tools.synth import GilbertElliott, p_frame_shards
+        from paper_2604_27441_b200.recovery import RecoveryEngine, pack_grid, stack_slots
 
-        S = len(stream_ids)
-        self.name, self.c, self.S = name, c, S
+        h, w = wl.h, wl.w
+        S = len(wl.ids)
+        self.name, self.c, self.S, self.h, self.w = name, c, S, h, w
         cfg = ModelConfig()
-        ck = Checkpoint.random_init(cfg, c, seed=0)          # torch.manual_seed(0) init
-        self.engine = RecoveryEngine(ck.build_model(precision=precision), precision)
+        if engine is None:
+            ck = Checkpoint.random_init(cfg, c, seed=0)          # torch.manual_seed(0) init
+            engine = RecoveryEngine(ck.build_model(precision=precision), precision)
+        self.engine = engine
         self.engine.model.native(device)
         F = cfg.stack_len
-        rng = np.random.default_rng(1000 * c)
-        # 6 planes per stream (5 refs + corrupted plane), slot = 6*s + i
-        self.host_frames = torch.empty((S * F, H, W, c), dtype=torch.uint8).pin_memory()
-        hf = self.host_frames.numpy()
-        for s in range(S):
-            base = rng.integers(0, 256, (H // 8 + 2, W // 8 + 2, c), dtype=np.uint8)
-            tex = np.kron(base, np.ones((8, 8, 1), np.uint8))
-            for i in range(F):
-                hf[s * F + i] = tex[i % 8: i % 8 + H, 0:W]      # slow drift
+        self.host_frames = torch.empty((S * F, h, w, c), dtype=torch.uint8).pin_memory()
+        hf = self.host_frames.numpy().reshape(S, F, h, w, c)
+        for s, sid in enumerate(wl.ids):
+            hf[s] = wl.planes(c, sid)
         self.frames = self.host_frames.to(device)
-        self.ring_view = self.frames.view(S, F, H, W, c)
-        self.host_planes = self.host_frames.view(S, F, H, W, c)[:, -1].contiguous().pin_memory()
+        self.ring_view = self.frames.view(S, F, h, w, c)
+        self.host_planes = self.host_frames.view(S, F, h, w, c)[:, -1].contiguous().pin_memory()
         self.index = torch.tensor([[s * F + i for i in stack_slots(5, 5, F)]
                                    for s in range(S)], dtype=torch.int32, device=device)
-        # loss-mask jobs: GE-dropped body shards of synthetic P-frame headers
-        jobs = []
-        for s, sid in enumerate(stream_ids):
-            ge = GilbertElliott(seed=sid + 17 * c)
-            hdr, nd, recv, enc = p_frame_shards(np.random.default_rng(sid + c),
-                                                W, H, c, L, ge.drop, present_ratio=0.1)
-            if recv.all():                     # ensure each stream needs recovery
-                recv[1 + (s % max(1, nd - 1))] = False
-            jobs.append(PFrameShards(hdr, nd, recv, L, enc))
-        self.jobs = jobs
-        nblk = (H // 16) * (W // 16)
-        self.lm = LossMaskBatch(S, max(len(j.header) for j in jobs) + 16,
-                                max(j.n_data for j in jobs) + 1, nblk, 1, device)
-        self.lm.stage(jobs)
-        self.lm.launch()
-        grids = self.lm.results()
+        nblk = (h // 16) * (w // 16)
+        self.jobs, self.lm = None, None
+        if wl.loss[0] in ("ge", "bern"):
+            self.jobs = []
+            for s, sid in enumerate(wl.ids):
+                hdr, nd, recv, enc = wl.job(c, L, s, sid)
+                self.jobs.append(PFrameShards(hdr, nd, recv, L, enc))
+            self.lm = LossMaskBatch(S, max(len(j.header) for j in self.jobs) + 16,
+                                    max(j.n_data for j in self.jobs) + 1, nblk, 1, device)
+            self.lm.stage(self.jobs)
+            self.lm.launch()
+            grids = self.lm.results()
+            self.wire = self.lm.wire
+        else:
+            grids = [wl.grid(c, sid) for sid in wl.ids]
+            bits = np.stack([pack_grid(g) for g in grids])
+            self.host_wire = torch.from_numpy(bits).pin_memory()
+            self.wire = self.host_wire.to(device)
         self.masked_patches = [int(g.sum()) for g in grids]
-        self.out = torch.empty((S, H, W, c), dtype=torch.uint8, device=device)
-        self.host_out = torch.empty((S, H, W, c), dtype=torch.uint8).pin_memory()
-        self.plane_bytes = H * W * c
-        # pipelined serving loop (public API) for the end-to-end number
-        from paper_2604_27441_b200.recovery import RecoveryPipeline
-        self.pipe = RecoveryPipeline(self.engine, S, H, W, L, self.lm.max_header,
-                                     self.lm.max_shards, self.ring_view[:, :cfg.k])
-        for buf in self.pipe.host_in:
-            buf.copy_(self.host_planes)           # the decoder writes planes here
+        self.out = torch.empty((S, h, w, c), dtype=torch.uint8, device=device)
+        self.host_out = torch.empty((S, h, w, c), dtype=torch.uint8).pin_memory()
+        self.pipe = None
+        if pipeline and self.jobs is not None:
+            from paper_2604_27441_b200.recovery import RecoveryPipeline
+            self.pipe = RecoveryPipeline(self.engine, S, h, w, L, self.lm.max_header,
+                                         self.lm.max_shards, self.ring_view[:, :cfg.k])
+            for buf in self.pipe.host_in:
+                buf.copy_(self.host_planes)           # the decoder writes planes here
+
+    def _mask(self, stream):
+        from paper_2604_27441_b200 import _native
+        import ctypes
+        if self.lm is not None:
+            _native.check(self.lm.lib.nvrec_loss_mask(ctypes.c_void_p(self.lm.dev_in.data_ptr()),
+                                                      self.lm.n,
+                                                      ctypes.c_void_p(int(stream.cuda_stream))))
 
     def device_step(self, stream):
         """Loss mask + recovery with inputs resident in HBM, merged in place
         (the serving mode of RecoveryPipeline: the recovered patches land in
         the corrupted plane's slot; the model never reads those pixels, so
         repeating the step recomputes the same plane)."""
-        from paper_2604_27441_b200 import _native
-        import ctypes
-        _native.check(self.lm.lib.nvrec_loss_mask(ctypes.c_void_p(self.lm.dev_in.data_ptr()),
-                                                  self.lm.n,
-                                                  ctypes.c_void_p(int(stream.cuda_stream))))
-        self.engine.recover_device(self.frames, self.index, self.lm.wire, in_place=True)
+        self._mask(stream)
+        self.engine.recover_device(self.frames, self.index, self.wire, in_place=True)
 
     def e2e_step(self, stream):
-        """Streaming in-process backend through pinned host buffers: the
-        receiver hands over each stream's decoded corrupted plane and its
-        loss-mask job (H2D); the k references are the device-resident ring
-        of earlier displayable planes; the recovered plane is pushed into the
-        ring (D2D) and returned to the host (D2H)."""
-        self.lm.launch(stream)                               # H2D jobs + kernel
+        """Unpipelined end to end: H2D of each stream's corrupted plane and
+        its loss-mask job (or mask bits), recovery against the device-resident
+        references, ring push (D2D), D2H of the recovered planes."""
+        if self.lm is not None:
+            self.lm.launch(stream)                           # H2D jobs + kernel
+        else:
+            self.wire.copy_(self.host_wire, non_blocking=True)
         self.ring_view[:, -1].copy_(self.host_planes, non_blocking=True)
-        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+        self.engine.recover_device(self.frames, self.index, self.wire, self.out)
         self.ring_view[:, -2].copy_(self.out, non_blocking=True)   # ring push
         self.host_out.copy_(self.out, non_blocking=True)
 
@@ -199,11 +324,12 @@ class ModalityWork:
         request ships the corrupted plane AND all k references (H2D)."""
         self.lm.launch(stream)
         self.frames.copy_(self.host_frames, non_blocking=True)
-        self.engine.recover_device(self.frames, self.index, self.lm.wire, self.out)
+        self.engine.recover_device(self.frames, self.index, self.wire, self.out)
         self.host_out.copy_(self.out, non_blocking=True)
 
     def h2d_bytes(self):
-        return int(self.lm.h2d_bytes + self.host_planes.numel())
+        m = self.lm.h2d_bytes if self.lm is not None else self.host_wire.numel()
+        return int(m + self.host_planes.numel())
 
     def h2d_bytes_protocol(self):
         return int(self.lm.h2d_bytes + self.host_frames.numel())
@@ -215,8 +341,8 @@ class ModalityWork:
 class ReceiverWork:
     """S streams of one modality as the receiver sees them: per frame time a
     codec P-frame (synthetic talking-motion content, encoded by the sender
-    restatement in synth.py) whose body shards went through the GE channel;
-    decoded + recovered on the GPU by ReceiverPipeline."""
+    restatement in tools/synth.py) whose body shards went through the GE
+    channel; decoded + recovered on the GPU by ReceiverPipeline."""
 
     def __init__(self, name, c, L, stream_ids, device, engine, n_frames=6):
         from tools import synth
@@ -257,6 +383,10 @@ class ReceiverWork:
         return self.pipe.submit([seq[j] for seq in self.seqs])
 
 
+def _events():
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
 def timed_receiver(rworks, steps, dist_on):
     """Receiver back end end to end: compressed P-frames in (pinned H2D),
     GPU decode + loss mask + recovery, displayable planes out (D2H)."""
@@ -264,8 +394,7 @@ def timed_receiver(rworks, steps, dist_on):
     torch.cuda.synchronize()
     if dist_on:
         torch.distributed.barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = _events()
     t0.record(main)
     for rw in rworks:
         rw.pipe.s_h2d.wait_event(t0)
@@ -278,12 +407,7 @@ def timed_receiver(rworks, steps, dist_on):
         main.wait_stream(rw.pipe.s_d2h)
     t1.record(main)
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if dist_on:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    return ms, h2d / steps
+    return max_over_ranks(t0.elapsed_time(t1), dist_on, "cuda"), h2d / steps
 
 
 def timed_pipeline(works, steps, dist_on):
@@ -296,25 +420,18 @@ def timed_pipeline(works, steps, dist_on):
     torch.cuda.synchronize()
     if dist_on:
         torch.distributed.barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = _events()
     t0.record(main)
     for wk in works:
         wk.pipe.s_h2d.wait_event(t0)
-    handles = []
     for _ in range(steps):
         for wk in works:
-            handles.append((wk, wk.pipe.submit(None, wk.jobs)))
+            wk.pipe.submit(None, wk.jobs)
     for wk in works:
         main.wait_stream(wk.pipe.s_d2h)
     t1.record(main)
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if dist_on:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    return ms
+    return max_over_ranks(t0.elapsed_time(t1), dist_on, "cuda")
 
 
 def run_steps(works, streams, fn, n, join_each_step=True):
@@ -348,17 +465,13 @@ def timed(works, streams, fn, steps, dist_on, join_each_step=True):
     if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = _events()
     t0.record()
     run_steps(works, streams, fn, steps, join_each_step)
     t1.record()
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
+    ms = max_over_ranks(t0.elapsed_time(t1), dist_on, "cuda")
     if dist_on:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
         torch.distributed.barrier()
     return ms
 
@@ -374,38 +487,62 @@ def attention_flops(ns, n_masked, nt=3, heads=2, hd=32, layers=2):
     return per_q * (ns * (layers - 1) + n_masked)
 
 
-class CpuReference:
-    """The reference CPU path (oracle restatement of RecoveryServer._recover,
-    fp32 torch-CPU with all host threads) on 720p RGB-D frames: random-init
-    weights (torch.manual_seed(0)), 10% block mask, k = 5 references."""
+# ----------------------------------------------------------------------------
+# reference CPU path (the oracle restatement; test infrastructure)
 
-    def __init__(self):
-        from oracle import nvrec_forward, recover as orec
+class CpuReference:
+    """The reference CPU path on a Workload's inputs: per stream-frame and
+    modality, the receiver/codec loss mask (oracle.lossmask, restating
+    receiver.py:224-237 + codec.py:250-281) and RecoveryServer._recover
+    (oracle.recover, server.py:181-196) in fp32 torch-CPU, with the same
+    random-init weights (seed 0) and planes as the GPU arm."""
+
+    def __init__(self, wl: Workload, threads=None):
+        from oracle import nvrec_forward, recover as orec, lossmask as olm
         from paper_2604_27441_b200.checkpoint import Checkpoint
         from paper_2604_27441_b200.config import ModelConfig
-        self.threads = os.cpu_count() or 1
+        self.threads = threads or (os.cpu_count() or 1)
         torch.set_num_threads(self.threads)
         self.arch = nvrec_forward.Arch()
-        self.orec = orec
-        rng = np.random.default_rng(3)
+        self.orec, self.olm, self.wl = orec, olm, wl
         self.states, self.inputs = {}, {}
-        for name, c, _ in MODS:
+        for name, c, L in MODS:
             ck = Checkpoint.random_init(ModelConfig(), c, seed=0)
             self.states[c] = {k: v.numpy() for k, v in ck.state.items()}
-            frames = rng.integers(0, 256, (6, H, W, c), dtype=np.uint8)
-            grid = rng.random((H // 16, W // 16)) < 0.1
-            self.inputs[c] = (frames[-1], grid, list(frames[:-1]))
+            per = []
+            for s, sid in enumerate(wl.ids):
+                fr = wl.planes(c, sid)
+                per.append((fr, wl.job(c, L, s, sid) if wl.loss[0] != "block" else wl.grid(c, sid), L))
+            self.inputs[c] = per
+        self.i = 0
 
     def frame(self):
-        """One RGB-D frame (both modalities)."""
+        """One stream's RGB-D frame (both modalities), round robin."""
+        s = self.i % len(self.wl.ids)
+        self.i += 1
         for _, c, _ in MODS:
-            plane, grid, refs = self.inputs[c]
-            self.orec.recover(self.states[c], self.arch, c, plane, grid, refs)
+            fr, m, L = self.inputs[c][s]
+            if isinstance(m, tuple):
+                hdr, nd, recv, enc = m
+                grid = self.olm.mask_from_shards(hdr, nd, set(np.flatnonzero(recv).tolist()), L, enc)
+            else:
+                grid = m
+            self.orec.recover(self.states[c], self.arch, c, fr[-1], grid, list(fr[:-1]))
 
 
-def cpu_reference(seconds, max_frames=None):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference(wl, seconds, threads=None, max_frames=None):
     """Frames/s of the reference CPU path over a bounded sample."""
-    ref = CpuReference()
+    ref = CpuReference(wl, threads)
     ref.frame()                               # warm-up
     n, t0 = 0, time.perf_counter()
     while True:
@@ -417,10 +554,15 @@ def cpu_reference(seconds, max_frames=None):
     return n / el, n, el, ref.threads
 
 
+def headline_workload(streams_total: int) -> Workload:
+    return Workload("720p_ge", H, W, range(streams_total), ("ge",))
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return
-    ref = CpuReference()
+    wl = headline_workload(args.streams_per_gpu * world)
+    ref = CpuReference(wl)
     for _ in range(args.warmup):
         ref.frame()
     t0 = time.perf_counter()
@@ -430,26 +572,79 @@ def reference_arm(args, rank, world):
     threads = ref.threads
     value = args.steps / tot
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "1280x720 RGB-D recovery (configs[2]); one RGB-D frame "
-                                   "per step (bounded sample of the 8-stream step), 10% block "
-                                   "mask, k=5 refs", "height": H, "width": W},
+            "config": {"workload": WORKLOAD_720P % args.streams_per_gpu,
+                       "streams_per_gpu": args.streams_per_gpu, "height": H, "width": W,
+                       "same_inputs_as_gpu_arm": True,
+                       "sample": "each step = one stream's RGB-D frame (round robin over the "
+                                 "%d streams): the same planes, GE-dropped shards and weights "
+                                 "as the GPU arm's step" % (args.streams_per_gpu * world)},
             "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads,
-                             "kind": "port",
-                             "sample": "%d x 720p RGB-D frames through the oracle "
-                                       "restatement of RecoveryServer._recover "
-                                       "(fp32 torch-CPU, %d threads)" % (args.steps, threads)},
+                             "kind": "port", "cpu_model": cpu_model(),
+                             "sample": "%d x 720p RGB-D stream-frames through the oracle "
+                                       "restatement of the receiver loss mask + "
+                                       "RecoveryServer._recover (fp32 torch-CPU, %d threads)"
+                                       % (args.steps, threads)},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def dry_run(args, rank, world):
+    """Launch / timing / reporting logic without a GPU (CPU tests)."""
+    dist_on = world > 1
+    if dist_on:
+        torch.distributed.init_process_group("gloo")
+    t0 = time.perf_counter()
+    x = torch.ones(1 << 16)
+    for _ in range(args.steps):
+        x = x * 1.0001
+    ms = max_over_ranks(1000 * (time.perf_counter() - t0), dist_on)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / max(1, args.steps),
+                          "streams_total": args.streams_per_gpu * world,
+                          "scaling": "weak"}), flush=True)
+    if dist_on:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------
+# our arm
+
+def measure_config(wl, device, precision, steps, warmup, dist_on, engines=None):
+    """Device-resident throughput + unpipelined e2e of one extra config."""
+    works = [ModalityWork(wl, n, c, L, device, precision,
+                          engine=engines[i] if engines else None)
+             for i, (n, c, L) in enumerate(MODS)]
+    streams = [torch.cuda.Stream(device) for _ in works]
+    run_steps(works, streams, "device_step", warmup)
+    ms = timed(works, streams, "device_step", steps, dist_on, join_each_step=False)
+    run_steps(works, streams, "e2e_step", 2)
+    ms_e2e = timed(works, streams, "e2e_step", steps, dist_on)
+    n = len(wl.ids) * steps
+    out = {"workload": wl.describe(), "value": n / (ms / 1e3),
+           "e2e_unpipelined": n / (ms_e2e / 1e3), "unit": "frames/s",
+           "ms_per_step": ms / steps,
+           "masked_patches_per_frame": {wk.name: float(np.mean(wk.masked_patches)) for wk in works},
+           "h2d_bytes_per_step": sum(wk.h2d_bytes() for wk in works),
+           "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works)}
+    del works
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
+    spawn_ranks(args)
     rank, world, local = dist_env()
     dist_on = world > 1
+    if args.dry_run:
+        dry_run(args, rank, world)
+        return
     if args.impl == "reference":
         if dist_on:
             torch.distributed.init_process_group("gloo")
@@ -466,20 +661,21 @@ def main():
     S = args.streams_per_gpu
     from paper_2604_27441_b200.sharding import streams_for_rank
     mine = streams_for_rank(S * world, rank, world)       # stream s -> GPU s mod N
-    works = [ModalityWork(n, c, L, mine, device=device, precision=args.precision)
+    wl = Workload("720p_ge", H, W, mine, ("ge",))
+    works = [ModalityWork(wl, n, c, L, device, args.precision, pipeline=True)
              for n, c, L in MODS]
     streams = [torch.cuda.Stream(device) for _ in works]
 
     # warm-up (both paths), then the device-resident timed region
     run_steps(works, streams, "device_step", args.warmup)
     run_steps(works, streams, "e2e_step", max(1, args.warmup // 2))
-    clocks = ClockSampler(local)
     # device throughput: modality streams run their steps back to back (the
     # e2e pipelines overlap the same way); the per-step-barrier figure is
     # reported beside it
-    ms = timed(works, streams, "device_step", args.steps, dist_on, join_each_step=False)
+    with ClockSampler(local) as clocks:
+        ms = timed(works, streams, "device_step", args.steps, dist_on, join_each_step=False)
+    clk = clocks.result()
     ms_joined = timed(works, streams, "device_step", args.steps, dist_on)
-    clk = clocks.stop()
     # end-to-end through host buffers (streaming backend) and the reference
     # wire-protocol variant that re-ships all k references every request
     for wk in works:                                         # pipeline warm-up
@@ -496,6 +692,7 @@ def main():
             rw.submit()
     torch.cuda.synchronize()
     ms_recv, recv_h2d = timed_receiver(rworks, args.steps, dist_on)
+    del rworks
     # per-stage device times: separate pass, both modalities serialised on ONE
     # stream so event brackets are not inflated by the concurrent modality
     torch.cuda.synchronize()
@@ -507,7 +704,8 @@ def main():
     # single-stream RGB-D latency (b = 1 per modality, e2e through host buffers)
     lat = []
     if rank == 0:
-        single = [ModalityWork(n, c, L, [999], device=device, precision=args.precision)
+        single_wl = Workload("720p_single", H, W, [999], ("ge",))
+        single = [ModalityWork(single_wl, n, c, L, device, args.precision)
                   for n, c, L in MODS]
         sst = [torch.cuda.Stream(device) for _ in single]
         run_steps(single, sst, "e2e_step", 5)
@@ -517,6 +715,46 @@ def main():
                    for _ in range(args.latency_iters)]
         lat_proto = [timed(single, sst, "protocol_step", 1, False)
                      for _ in range(args.latency_iters)]
+        del single
+
+    # the other BASELINE configs and densities (device value + unpipelined e2e)
+    extra, fast = {}, None
+    if not args.no_extra:
+        k = max(5, args.steps // 10)
+        other = "fast" if args.precision == "precise" else "precise"
+        # the other precision on the headline workload
+        wk2 = [ModalityWork(wl, n, c, L, device, other, pipeline=True) for n, c, L in MODS]
+        st2 = [torch.cuda.Stream(device) for _ in wk2]
+        run_steps(wk2, st2, "device_step", args.warmup)
+        ms2 = timed(wk2, st2, "device_step", args.steps, dist_on, join_each_step=False)
+        for wk in wk2:
+            for _ in range(3):
+                wk.pipe.submit(None, wk.jobs)
+        torch.cuda.synchronize()
+        ms2_e2e = timed_pipeline(wk2, args.steps, dist_on)
+        n2 = S * world * args.steps
+        fast = {"precision": other, "dtype": "bf16" if other == "fast" else PRECISE_DTYPE,
+                "value": n2 / (ms2 / 1e3), "unit": "frames/s", "ms_per_step": ms2 / args.steps,
+                "e2e": {"value": n2 / (ms2_e2e / 1e3), "unit": "frames/s",
+                        "h2d_bytes_per_step": sum(w.pipe.h2d_bytes() for w in wk2),
+                        "d2h_bytes_per_step": sum(w.pipe.d2h_bytes() for w in wk2)},
+                "note": "same workload and timing as the headline, %s operands" %
+                        ("bf16/fp16 tensor-core (max-abs 2.6e-4 at 720p)" if other == "fast"
+                         else "split (fp32-class)")}
+        del wk2
+        torch.cuda.empty_cache()
+        engines = [w.engine for w in works]
+        cfgs = [
+            ("configs[0] 320x240 10% block", Workload("c0", 240, 320, mine, ("block", 0.10))),
+            ("configs[1] 640x480 Bernoulli 5%", Workload("c1", 480, 640, mine, ("bern", 0.05))),
+            ("configs[2] 720p 10% block", Workload("c2b10", H, W, mine, ("block", 0.10))),
+            ("configs[2] 720p 20% block", Workload("c2b20", H, W, mine, ("block", 0.20))),
+            ("configs[3] 1920x1088 20% block", Workload("c3", 1088, 1920, mine, ("block", 0.20))),
+            ("configs[4] 64 streams x 720p GE on this GPU",
+             Workload("c4", H, W, streams_for_rank(64, rank, world), ("ge",))),
+        ]
+        for key, cwl in cfgs:
+            extra[key] = measure_config(cwl, device, args.precision, k, 2, dist_on, engines)
 
     if dist_on:
         torch.distributed.barrier()
@@ -548,11 +786,11 @@ def main():
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "attn_tc_ncu.json")
     if os.path.exists(tpath):
-        tj = json.load(open(tpath))
+        tj = json.load(open(tpath)).get(args.precision, {})
         traffic = tj.get("dram_bytes_per_launch")
         traffic_src = tj.get("source")
-    step_ms_prof = sum(prof.ms.values()) / args.steps
     launches_per_step = prof.total_launches / args.steps
+    precise = args.precision == "precise"
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -561,13 +799,14 @@ def main():
                       "streams join at the end (as the e2e pipelines run); "
                       "value_frame_barrier: both modalities finish step t before t+1 starts",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16" if (args.precision == "fast" and prof.launches["attn_tc"]) else "f32",
+        "dtype": PRECISE_DTYPE if precise else "bf16",
+        "precision": PRECISE_NOTE if precise else "fast: bf16/fp16 tensor-core operands, fp32 "
+                                                  "accumulation (720p max-abs 2.6e-4)",
         "data": "synthetic",
-        "config": {"workload": "1280x720 RGB-D streams (configs[2] x configs[4]): %d "
-                               "streams/GPU, GE loss (p_gb=0.0155,p_bg=0.5) on body shards of "
-                               "synthetic P-frame headers, k=5 refs" % S,
+        "config": {"workload": WORKLOAD_720P % S,
                    "streams_per_gpu": S, "height": H, "width": W,
                    "precision": args.precision,
+                   "same_inputs_as_reference_arm": True,
                    "masked_patches_per_frame": {wk.name: float(np.mean(wk.masked_patches))
                                                 for wk in works},
                    "l2": "inputs larger than L2 (%.0f MB of u8 planes per step > 126 MB)"
@@ -592,14 +831,14 @@ def main():
                                  "per request (recovery.py:219-227)"},
         "e2e_receiver": {"value": S * world * args.steps / (ms_recv / 1000.0), "unit": "frames/s",
                          "h2d_bytes_per_step": int(recv_h2d),
-                         "d2h_bytes_per_step": sum(rw.pipe.d2h_bytes() for rw in rworks),
+                         "d2h_bytes_per_step": sum(wk.d2h_bytes() for wk in works),
                          "path": "ReceiverPipeline: per step each stream's received P-frame "
                                  "(codec header + assembled body with zero-filled lost "
                                  "shards, receiver.py:222-237) H2D, nvrec_decode (zero-fill "
                                  "decode + loss mask, codec.py:260-321) against the newest "
                                  "ring plane, nvrec_recover_u8 into the ring, D2H of the "
                                  "displayable planes; synthetic talking-motion 720p content "
-                                 "encoded by the synth.py sender, GE channel loss"},
+                                 "encoded by the tools/synth.py sender, GE channel loss"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "p50_latency_ms": statistics.median(lat),
         "p99_latency_ms": float(np.percentile(lat, 99)),
@@ -614,7 +853,8 @@ def main():
         "stage_ms_per_step": {k: v / args.steps for k, v in prof.ms.items() if v},
         "stage_note": "per-stage device ms from CUDA-event brackets, both modalities "
                       "serialised on one stream (separate pass)",
-        "roofline": {"kernel": att_kind, "bound": "tensor", "achieved": achieved,
+        "roofline": {"kernel": att_kind + (" (split-bf16 x3)" if precise else ""),
+                     "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "binding_unit": "mufu (SFU ex2): head_dim 32 gives 128 MMA-FLOP per "
                                      "exponential, so the exp rate, not the tensor core, "
@@ -626,18 +866,33 @@ def main():
                               "frac": (exps / (att_ms / 1000.0) / MUFU_PEAK) if att_ms else 0.0,
                               "note": "binding unit for head_dim 32 (128 MMA-FLOP per exp); "
                                       "peak = 148 SM x 16 ex2/clk x 1.965 GHz (15.9 ex2/clk/SM "
-                                      "measured by tools/ubench_xu.cu); 1/4 of the exps run as "
-                                      "FMA-pipe polynomials"},
+                                      "measured by tools/ubench_xu.cu); " +
+                                      ("all exps on MUFU (fp32-accurate ex2.approx)" if precise
+                                       else "1/4 of the exps run as FMA-pipe polynomials")},
+                     "algorithmic_note": "achieved counts the reference-equivalent (pruned) "
+                                         "attention FLOPs, not the 3x MMA work of the split "
+                                         "products" if precise else "reference-equivalent "
+                                         "(pruned) attention FLOPs",
                      "share_of_step": att_ms / max(1e-9, sum(prof.ms.values())),
                      "algorithmic_flops_per_launch": flops / max(1, att_launches)},
     }
+    if fast is not None:
+        line["other_precision"] = fast
+    if extra:
+        line["configs"] = extra
     if not args.no_cpu_baseline:
-        fps, n, el, threads = cpu_reference(args.cpu_seconds)
+        fps, n, el, threads = cpu_reference(wl, args.cpu_seconds)
+        fps1, n1, el1, _ = cpu_reference(wl, min(6.0, args.cpu_seconds / 2), threads=1,
+                                         max_frames=3)
+        torch.set_num_threads(os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": threads,
-                                "kind": "port",
-                                "sample": "%d x 720p RGB-D frames (%.1f s) through the oracle "
-                                          "restatement of RecoveryServer._recover, fp32 "
-                                          "torch-CPU, %d threads" % (n, el, threads)}
+                                "kind": "port", "cpu_model": cpu_model(),
+                                "sample": "%d x 720p RGB-D stream-frames of the headline "
+                                          "workload (%.1f s) through the oracle restatement of "
+                                          "the receiver loss mask + RecoveryServer._recover, "
+                                          "fp32 torch-CPU, %d threads" % (n, el, threads),
+                                "threads_1": {"value": fps1, "unit": "frames/s", "cores": 1,
+                                              "sample": "%d stream-frames (%.1f s)" % (n1, el1)}}
     print(json.dumps(line), flush=True)
     if dist_on:
         torch.distributed.destroy_process_group()

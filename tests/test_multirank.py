@@ -59,3 +59,39 @@ def test_route_preserves_stream_order():
         for sid in {s for s, _ in items}:
             seq = [i for s, i in items if s == sid]
             assert seq == sorted(seq)
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """``bench.py --gpus 2`` outside torchrun re-launches itself with two
+    ranks (torch.distributed.run, 127.0.0.1) and reports n_gpus = 2 from the
+    max-over-ranks timing path (--dry-run: gloo, no GPU work)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--dry-run", "--steps", "3"], capture_output=True, text=True,
+                         timeout=300, check=True).stdout
+    line = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["streams_total"] == 16 and line["scaling"] == "weak"
+
+
+def test_reference_arm_uses_the_gpu_arm_inputs():
+    """The CPU reference arm and the GPU arm build their inputs from the same
+    deterministic Workload (planes, GE-dropped shards): same_config."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import numpy as np
+    import bench
+    a = bench.Workload("t", 64, 96, range(3), ("ge",))
+    b = bench.Workload("t", 64, 96, range(3), ("ge",))
+    for c, L in ((3, 1024), (1, 512)):
+        for s in range(3):
+            assert np.array_equal(a.planes(c, s), b.planes(c, s))
+            ja, jb = a.job(c, L, s, s), b.job(c, L, s, s)
+            assert ja[0] == jb[0] and ja[1] == jb[1] and np.array_equal(ja[2], jb[2])
+            assert not ja[2].all()                     # every stream needs recovery
+    ref = bench.CpuReference(a, threads=2)
+    ref.frame()
+    ref.frame()
