@@ -58,6 +58,19 @@ __device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe: has the phase with parity `parity` of `bar` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // ---- warpgroup register reallocation ----------------------------------------
 template <uint32_t kRegs>
 __device__ __forceinline__ void setmaxnreg_inc() {
