@@ -16,7 +16,9 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libnvrec_b200.so")
+# NVREC_LIB: an alternative in-tree build of the same library (trace /
+# experiment variants, tools/); the default is the product build
+LIB_PATH = os.environ.get("NVREC_LIB") or os.path.join(_HERE, "lib", "libnvrec_b200.so")
 
 PREC_FAST = 0
 PREC_PRECISE = 1

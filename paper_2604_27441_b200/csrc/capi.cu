@@ -886,6 +886,11 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
   return 0;
 }
 
+#ifdef NVREC_TRACE
+// trace build only (not in include/nvrec_b200.h): phase timestamps of one CTA
+int nvrec_debug_attn_trace(unsigned long long* host, int n) { return nvrec::attn_trace(host, n); }
+#endif
+
 int64_t nvrec_attn_fixup_items(void) {
   const int64_t n = nvrec::attn_fixup_items();
   if (n < 0) return fail(NVREC_E_CUDA, "reading the fix-up counter failed");

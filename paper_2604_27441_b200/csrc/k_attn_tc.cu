@@ -92,6 +92,7 @@ constexpr uint32_t kKBytes = kTileK * kHd * 2;         // 8 KB
 constexpr uint32_t kVBytes = kHd * kTileK * 2;         // 8 KB
 constexpr uint32_t kIdescS = idesc_bf16(128, 128);
 constexpr uint32_t kIdescPV = idesc_bf16(128, 32);
+constexpr uint32_t kIdescPV64 = idesc_bf16(128, 64);
 constexpr uint32_t kColOp = 64;                        // O'(j) inside its S buffer
 constexpr float kSlackSum = 256.f;                     // speculative-max headroom: row sum of P
 static_assert(2 * 2 * kTileK <= 512, "TMEM budget");
@@ -643,6 +644,308 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
   pdl_trigger();
 }
 
+// ---- dense split-bf16 attention with 128-key tiles (precise path) -------------
+// The dense speculative launch of the precise path: same arithmetic as the
+// kX3 variant of attn_tc_kernel, but 128-key tiles.  A split P fills its whole
+// 128-column S buffer (per 64-key chunk h: P_hi pairs at 64h + [0,32), P_lo
+// pairs at 64h + [32,64)), so the two query tiles share THREE rotating S
+// buffers: S tile n (query tile t = n % ntq, key tile j = n / ntq) lives in
+// buffer n % 3, and the MMA issuer runs PV two S tiles behind, i.e. the next S
+// of a query tile is issued as soon as the OTHER tile's previous P is done --
+// each softmax warpgroup finds its next S computed while it works.  O'(t) has
+// its own 64 columns (Ph [Vh | Vl] as one N = 64 MMA, then Pl Vh into the
+// first half; the fold adds the halves); TMEM = 3 x 128 + 2 x 64 = 512 columns.
+// Twice the keys per mbarrier round trip / O' fold of the 64-key variant.
+constexpr int kWTK = 128, kWStages = 4;
+#ifdef NVREC_TRACE
+// phase timestamps of one CTA (tools/trace_attn.py): role r (0: softmax warp
+// 0 = tile 0, 1: softmax warp 4 = tile 1, 2: MMA issuer), step i, event e
+constexpr int kTraceCta = 300;
+__device__ unsigned long long g_trace[3 * 128 * 8];
+#define NVREC_TR(role, i, e)                                                          \
+  do {                                                                                \
+    if (blockIdx.x == kTraceCta && (i) < 128) g_trace[((role) * 128 + (i)) * 8 + (e)] = clock64(); \
+  } while (0)
+#else
+#define NVREC_TR(role, i, e) do {} while (0)
+#endif
+constexpr uint32_t kWQBytes = 128 * 128, kWKBytes = 128 * 128, kWVBytes = 128 * 128;
+
+struct __align__(1024) SmemW {
+  uint8_t v[kWStages][kWVBytes];    // V^T: two (64 keys x 64 rows) boxes, rows 0-31 hi, 32-63 lo
+  uint8_t q[2][kWQBytes];           // Q tile [128][64] bf16 (hi | lo), SWIZZLE_128B
+  uint8_t k[kWStages][kWKBytes];    // K tile [128][64]
+  uint64_t q_full, kv_full[kWStages], kv_empty[kWStages];
+  uint64_t s_full[3], p_full[2], pv_full[2];
+  int redo;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(threads_for(2), 1)
+attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_v, TcArgs a) {
+  pdl_wait();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SmemW& sm = *reinterpret_cast<SmemW*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkv_all = (a.ns + kWTK - 1) / kWTK;
+  const int it = int(blockIdx.x);
+  const int seq = it % a.seqs, split = (it / a.seqs) % a.splits, group = it / (a.seqs * a.splits);
+  const int b = seq / (a.nt * a.heads);
+  const int nq = a.ns;
+  const int j0 = split * nkv_all / a.splits;
+  const int nkv = (split + 1) * nkv_all / a.splits - j0;
+  const int q0 = group * 2 * kTileQ;
+  if (q0 >= nq) return;
+  const int ntq = min(2, (nq - q0 + kTileQ - 1) / kTileQ);
+  const int N = nkv * ntq;                                  // S tiles of this CTA
+  constexpr uint32_t kOCol = 3 * kWTK;                      // O'(t) at 384 + 32 t
+  constexpr int kProducer = 8, kMma = 9;
+  if (warp == kProducer && lane == 0) {
+    sm.redo = a.mode == 2 ? 1 : 0;
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int i = 0; i < 3; ++i) mbar_init(&sm.s_full[i], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.pv_full[t], 1);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+  }
+  if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp >= 8) {
+    setmaxnreg_dec<kRegsCtl>();
+    if (warp == kProducer && lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      mbar_expect_tx(&sm.q_full, ntq * kWQBytes);
+      for (int t = 0; t < ntq; ++t) tma_load_3d(sm.q[t], &tm_q, &sm.q_full, 0, q0 + t * kTileQ, seq);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % kWStages;
+        mbar_wait(&sm.kv_empty[s], ((j / kWStages) & 1) ^ 1);
+        mbar_expect_tx(&sm.kv_full[s], kWKBytes + kWVBytes);
+        const int key0 = (j0 + j) * kWTK;
+        tma_load_3d(sm.k[s], &tm_k, &sm.kv_full[s], 0, key0, seq);
+        tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], key0, 0, seq);
+        tma_load_3d(sm.v[s] + kWVBytes / 2, &tm_v, &sm.kv_full[s], key0 + 64, 0, seq);
+      }
+    } else if (warp == kMma && lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      const uint32_t qbase = smem_u32(sm.q[0]);
+      constexpr uint32_t idS = idesc_bf16(128, kWTK);
+      mbar_wait(&sm.q_full, 0);
+      for (int n = 0; n < N + 2; ++n) {
+        NVREC_TR(2, n, 0);
+        if (n < N) {
+          // S(n) -> buffer n % 3 (its previous user, PV(n-3), was issued in
+          // iteration n-1: the tensor pipe executes MMAs in issue order)
+          const int t = n % ntq, j = n / ntq, s = j % kWStages;
+          if (t == 0) {
+            mbar_wait_fast(&sm.kv_full[s], (j / kWStages) & 1);
+            tc_fence_after();
+          }
+          const uint32_t kb = smem_u32(sm.k[s]), qb = qbase + t * kWQBytes;
+          const uint32_t sc = tmem + (n % 3) * kWTK;
+          constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
+#pragma unroll
+          for (int u = 0; u < 6; ++u)
+            mma_ss(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
+                   sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
+          mma_commit(&sm.s_full[n % 3]);
+        }
+        NVREC_TR(2, n, 1);
+        const int m = n - 2;
+        if (m >= 0 && m < N) {
+          // O'_t(m) = Ph Vh + Ph Vl + Pl Vh over 8 K16 chunks
+          const int t = m % ntq, j = m / ntq, s = j % kWStages;
+          mbar_wait_fast(&sm.p_full[t], j & 1);
+          NVREC_TR(2, n, 2);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sm.v[s]);
+          const uint32_t bc = tmem + (m % 3) * kWTK, oc = tmem + kOCol + 64 * t;
+          // per 16 keys: Ph [Vh | Vl] (one N = 64 MMA: the V^T hi and lo rows
+          // are adjacent) + Pl Vh (N = 32); O'(t) = D[0,32) + D[32,64)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
+            const uint32_t vh = vb + (kk >> 2) * (kWVBytes / 2) + (kk & 3) * 32;
+            mma_ts(oc, ah, sdesc(vh, 1024, kSwizzle128B), kIdescPV64, kk);
+            mma_ts(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
+          }
+          mma_commit(&sm.pv_full[t]);
+          if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);     // K/V(j) fully consumed
+        }
+        NVREC_TR(2, n, 3);
+      }
+    }
+  } else {
+    setmaxnreg_inc<regs_softmax(2)>();
+    // ------------------------------------------------------------ softmax warps
+    const int t = warp >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    float m = -INFINITY, l = 0.f, a_prev = 0.f;
+    float2 o2[kHd / 2];
+#pragma unroll
+    for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
+    const bool live_t = t < ntq;
+    const bool rows_live = live_t && q0 + t * kTileQ + quarter * 32 < nq;
+    const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
+    auto fold = [&](int j) {                  // O'(t) of key tile j: both halves
+      mbar_wait(&sm.pv_full[t], j & 1);
+      tc_fence_after();
+      uint32_t ov[64];
+      tmem_ld32(tmem + lane_off + kOCol + 64 * t, ov);
+      tmem_ld32(tmem + lane_off + kOCol + 64 * t + 32, ov + 32);
+      tmem_wait_ld();
+      const float2 ap = make_float2(a_prev, a_prev);
+#pragma unroll
+      for (int e = 0; e < kHd / 2; ++e) {
+        const float2 d = fadd2(make_float2(__uint_as_float(ov[2 * e]), __uint_as_float(ov[2 * e + 1])),
+                               make_float2(__uint_as_float(ov[32 + 2 * e]),
+                                           __uint_as_float(ov[33 + 2 * e])));
+        o2[e] = ffma2(o2[e], ap, d);
+      }
+    };
+    const bool tr = quarter == 0 && lane == 0;
+    for (int j = 0; live_t && j < nkv; ++j) {
+      const int n = j * ntq + t;
+      const uint32_t t_s = tmem + lane_off + (n % 3) * kWTK;
+      if (tr) NVREC_TR(t, j, 0);
+      mbar_wait(&sm.s_full[n % 3], (n / 3) & 1);
+      if (tr) NVREC_TR(t, j, 1);
+      tc_fence_after();
+      const int valid = a.ns - (j0 + j) * kWTK;
+      float mn = m;
+      if (j == 0 && rows_live) {
+        // exact max over the first key tile; speculative afterwards
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t r[64];
+          tmem_ld32(t_s + 64 * h, r);
+          tmem_ld32(t_s + 64 * h + 32, r + 32);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            mx4[c & 3] = fmaxf(mx4[c & 3], 64 * h + c < valid ? __uint_as_float(r[c]) : -INFINITY);
+        }
+        mn = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2);
+      }
+      float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 nm2 = make_float2(-mn, -mn);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (rows_live) {
+          uint32_t r[64], pl[32];
+          tmem_ld32(t_s + 64 * h, r);
+          tmem_ld32(t_s + 64 * h + 32, r + 32);
+          tmem_wait_ld();
+          if (valid < kWTK) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              if (64 * h + c >= valid) r[c] = __float_as_uint(-INFINITY);
+          }
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float2 v = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
+            const float2 p = make_float2(ex2(v.x), ex2(v.y));
+            sum2[(c >> 1) & 1] = fadd2(sum2[(c >> 1) & 1], p);
+            split_bf16(p.x, p.y, r[c >> 1], pl[c >> 1]);   // r[c/2] already consumed
+          }
+          tmem_st16(t_s + 64 * h, r);
+          tmem_st16(t_s + 64 * h + 16, r + 16);
+          tmem_st16(t_s + 64 * h + 32, pl);
+          tmem_st16(t_s + 64 * h + 48, pl + 16);
+        }
+        if (tr) NVREC_TR(t, j, 2 + 2 * h);
+        if (h == 0 && j > 0) fold(j - 1);
+        if (tr && h == 0) NVREC_TR(t, j, 3);
+      }
+      float2 sums = fadd2(sum2[0], sum2[1]);
+      float tsum = sums.x + sums.y;
+      if (j > 0 && __any_sync(0xffffffffu, !(tsum <= kSlackSum))) {
+        // rare: rescale this row's P (hi and lo) by 2^-k, exact
+        tmem_wait_st();
+        float pmax = 0.f;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[32];
+          tmem_ld32(t_s + 64 * h, pk);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float2 pv = unpack_bf16(pk[c]);
+            pmax = fmaxf(pmax, fmaxf(pv.x, pv.y));
+          }
+        }
+        if (!(tsum <= kSlackSum) && !(pmax < 0x1p100f)) sm.redo = 1;
+        const float k = tsum > kSlackSum && pmax < 0x1p100f ? fmaxf(0.f, ceilf(__log2f(pmax))) : 0.f;
+        const float f = ex2(-k);
+#pragma unroll 1
+        for (int g4 = 0; g4 < 4; ++g4) {        // hi and lo column groups alike
+          uint32_t pk[32];
+          tmem_ld32(t_s + 32 * g4, pk);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float2 pv = unpack_bf16(pk[c]);
+            pk[c] = pack_bf16(pv.x * f, pv.y * f);
+          }
+          tmem_st32(t_s + 32 * g4, pk);
+        }
+        tsum *= f;
+        mn += k;
+      }
+      const float alpha = ex2(m - mn);
+      l = l * alpha + tsum;
+      m = mn;
+      a_prev = alpha;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full[t]);
+      if (tr) NVREC_TR(t, j, 5);
+    }
+    if (live_t) {
+      fold(nkv - 1);
+      const int q = q0 + t * kTileQ + row;
+      if (q < nq && a.splits > 1) {
+        float* dst = a.part + ((size_t(split) * a.seqs + seq) * a.ns + q) * kPart;
+#pragma unroll
+        for (int e = 0; e < kHd / 2; e += 2)
+          *reinterpret_cast<float4*>(dst + 2 * e) = make_float4(o2[e].x, o2[e].y, o2[e + 1].x, o2[e + 1].y);
+        dst[32] = m;
+        dst[33] = l;
+      } else if (q < nq) {
+        const int it2 = (seq / a.heads) % a.nt, hh = seq % a.heads;
+        const float inv = 1.f / l;
+        float4* dst = reinterpret_cast<float4*>(a.ao + (size_t(b * a.nt + it2) * a.ns + q) * a.d + hh * kHd);
+#pragma unroll
+        for (int e = 0; e < kHd / 2; e += 2)
+          dst[e / 2] = make_float4(o2[e].x * inv, o2[e].y * inv, o2[e + 1].x * inv, o2[e + 1].y * inv);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == kProducer && lane == 0 && sm.redo != 0) {
+    const int idx = atomicAdd(a.redo_list, 1);     // overflowed: exact fix-up later
+    a.redo_list[2 + idx] = it;
+  }
+  pdl_trigger();
+}
+
 // Merge the key-range partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 // One thread per (row, output dim); 8 rows per 256-thread block, grid-stride.
 __global__ void __launch_bounds__(256)
@@ -704,6 +1007,14 @@ bool make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 
 bool tc_supported(const Dims& D) { return D.hd == kHd; }
 
+#ifdef NVREC_TRACE
+int attn_trace(unsigned long long* host, int n) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int m = n < int(sizeof(g_trace) / 8) ? n : int(sizeof(g_trace) / 8);
+  return cudaMemcpyFromSymbol(host, g_trace, m * 8) == cudaSuccess ? m : -1;
+}
+#endif
+
 int64_t attn_fixup_items() {
   unsigned long long v = 0;
   if (cudaDeviceSynchronize() != cudaSuccess ||
@@ -740,6 +1051,19 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
                      Geo<true>::TK, 2 * kHd, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
+  // the dense precise launch runs attn_x3w_kernel (128-key tiles, K boxes of
+  // 128 rows); NVREC_ATTN_X3W=0 keeps the 64-key variant (A/B)
+  static int wide_env = -1;
+  if (wide_env < 0) {
+    const char* e = getenv("NVREC_ATTN_X3W");
+    wide_env = e && e[0] == '0' ? 0 : 1;
+  }
+  const bool wide = x3 && !count && wide_env;
+  CUtensorMap tkw;
+  if (wide && !make_map_3d(&tkw, A.kh, 2 * kHd, A.ns, seqs, 2 * kHd * 2,
+                           uint64_t(A.ns_pad) * 2 * kHd * 2, 2 * kHd, kWTK,
+                           CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   TcArgs ta;
   ta.ao = A.ao;
   ta.ao_half = ao_half;
@@ -759,7 +1083,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   // range (flash-decoding partials merged by attn_combine_kernel) so every
   // SM slot works.
   const int qt = count ? 1 : 2, per_sm = count ? 2 : 1;
-  const int nkv = ceil_div(A.ns, x3 ? Geo<true>::TK : kTileK);
+  const int nkv = ceil_div(A.ns, x3 && !wide ? Geo<true>::TK : kTileK);
   ta.groups = count ? 1 : ceil_div(A.ns, qt * kTileQ);
   int best = 1;
   double best_t = 1e30;
@@ -799,6 +1123,12 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
     if (mode == 1 || !A.redo_list) {
       // exact maxima throughout (tests), or no fix-up list available
       launch_seq(k_exact, grid, nth, smem, s, tq, tk, tv, ta);
+    } else if (X3 && QT == 2 && wide) {
+      // dense precise launch: 128-key tiles, rotating S buffers
+      const size_t sw = sizeof(SmemW) + 1024;
+      if ((err = smem_optin(attn_x3w_kernel, int(sw))) != cudaSuccess) return;
+      launch_seq(attn_x3w_kernel, grid, nth, sw, s, tq, tkw, tv, ta);
+      launch_pdl(k_fix, kFixCtas, nth, smem, s, tq, tk, tv, ta);
     } else {
       launch_seq(k_spec, grid, nth, smem, s, tq, tk, tv, ta);
       // exact fix-up of the (rare) items whose speculative exponent overflowed:

@@ -130,6 +130,9 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
                            int* splits_out = nullptr, bool ao_half = false,
                            bool x3 = false);
 int64_t attn_fixup_items();   // -1 on a CUDA error
+#ifdef NVREC_TRACE
+int attn_trace(unsigned long long* host, int n);   // trace build (tools/trace_attn.py)
+#endif
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
                             const uint8_t* refs, const uint8_t* mask_bits, uint8_t* out,
