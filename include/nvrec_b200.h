@@ -226,8 +226,8 @@ enum {
   NVREC_STAGE_LOSSMASK = 0, NVREC_STAGE_MASKLIST = 1, NVREC_STAGE_COPY = 2,
   NVREC_STAGE_EMBED = 3, NVREC_STAGE_LNQKV = 4, NVREC_STAGE_ATTN_SIMT = 5,
   NVREC_STAGE_ATTN_TC = 6, NVREC_STAGE_TOKEN = 7, NVREC_STAGE_BASELINE = 8,
-  NVREC_STAGE_DECODE = 9, NVREC_STAGE_RS = 10,
-  NVREC_NUM_STAGES = 11
+  NVREC_STAGE_DECODE = 9, NVREC_STAGE_RS = 10, NVREC_STAGE_LAST_TC = 11,
+  NVREC_NUM_STAGES = 12
 };
 int nvrec_profile_begin(void);
 int nvrec_profile_end(float* ms_per_stage, int32_t* launches_per_stage, int32_t n_stages);

@@ -33,7 +33,7 @@ EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct",
            "nvrec_attn_fixup_items")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
-          "token", "baseline", "decode", "rs")
+          "token", "baseline", "decode", "rs", "last_tc")
 ABI_VERSION = 4
 
 

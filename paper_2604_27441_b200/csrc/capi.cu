@@ -185,6 +185,14 @@ bool precise_simt() {
   return on;
 }
 
+bool last_simt() {
+  static const bool on = [] {
+    const char* e = getenv("NVREC_LAST_SIMT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int attn_mode(const Dims& D, int precision) {
   if (!nvrec::tc_supported(D)) return 0;
   return precision == NVREC_PREC_FAST ? 1 : 2;
@@ -286,11 +294,17 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
     const bool tc_tail = !last && nvrec::token_tc_supported(D) &&
                          (fast ? m->W.tc.blk[li] != nullptr
                                : (am == 2 && m->W.tc.blk3[li] != nullptr && !precise_simt()));
+    // tensor-core last block + head (k_last_tc.cu); NVREC_LAST_SIMT=1 keeps the
+    // CUDA-core token_kernel (A/B)
+    const bool last_tc = last && am != 0 && m->W.tc.last3 != nullptr && !precise_simt() &&
+                         !last_simt() && nvrec::last_tc_supported(D, b);
     if (am) {
       ProfScope ps(NVREC_STAGE_ATTN_TC, s);
       int nk = 1;
-      // the SIMT token kernel merges key-split partials itself
-      const bool defer = !tc_tail;
+      // the SIMT token kernel merges key-split partials itself; the tensor-core
+      // last block reads merged rows (attn_combine_kernel: one thread per
+      // element instead of a serial per-row merge on the last block's lanes)
+      const bool defer = !tc_tail && !last_tc;
       e = nvrec::launch_attn_tc(A, D, prune_here ? A.count : nullptr, s, &nk, defer, &splits,
                                 fast && tc_tail,   // token_tc reads ao as fp16
                                 am == 2);
@@ -325,7 +339,33 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
     ta.out_slot = ip.frame_index ? ip.frame_index + (D.F - 1) : nullptr;
     ta.slot_stride = D.F;
     ta.frame_bytes = size_t(h) * w * D.c;
-    if (tc_tail && am == 2) {
+    if (last_tc) {
+      const nvrec::BlockW& bw = m->W.blk[li];
+      nvrec::LastTcArgs la{};
+      la.b = b; la.ns = A.ns; la.nt = D.nt; la.c = D.c;
+      la.img_h = h; la.img_w = w; la.nw = A.nw;
+      la.list = ta.list;
+      la.count = ta.list ? A.count : nullptr;
+      la.x = A.x; la.ao = A.ao;
+      la.w_blk = m->W.tc.last3;
+      la.w_head = m->W.tc.head3;
+      for (int j = 0; j < 5; ++j) la.sc[j] = m->W.tc.sc_blk[li][j];
+      la.sc_head = m->W.tc.sc_head;
+      la.b_proj_s = bw.proj_s_b; la.ln_t_w = bw.ln_t_w; la.ln_t_b = bw.ln_t_b;
+      la.b_qkv_t = bw.qkv_t_b; la.b_proj_t = bw.proj_t_b; la.ln_m_w = bw.ln_m_w;
+      la.ln_m_b = bw.ln_m_b; la.b_fc1 = bw.fc1_b; la.b_fc2 = bw.fc2_b;
+      la.norm_w = m->W.norm_w; la.norm_b = m->W.norm_b; la.head_b = m->W.head_b;
+      la.out_f32 = out_f32; la.out_u8 = out_u8;
+      la.out_frames = ip.frames; la.out_slot = ta.out_slot;
+      la.slot_stride = D.F; la.frame_bytes = ta.frame_bytes;
+      static const int hs_env = [] {
+        const char* e = getenv("NVREC_LAST_HSPLIT");   // A/B: CTAs per tile cap
+        return e ? atoi(e) : 4;
+      }();
+      la.max_hsplit = hs_env;
+      ProfScope ps(NVREC_STAGE_LAST_TC, s);
+      e = nvrec::launch_last_tc(la, b * A.ns, s);
+    } else if (tc_tail && am == 2) {
       const nvrec::BlockW& bw = m->W.blk[li];
       const nvrec::BlockW& bn = m->W.blk[li + 1];
       nvrec::TokenX3Args tt{};
@@ -465,6 +505,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
   const size_t base_row = size_t(T - 1) * p * p * c;
   for (int k = 0; k < d; ++k)
     for (int u = 0; u < D.used; ++u) h.push_back(hw[(base_row + u) * d + k]);
+  while (h.size() % 4) h.push_back(0.f);   // head_b read as float4 (k_last_tc.cu)
   mark();  // 8 head_b
   for (int u = 0; u < D.used; ++u) h.push_back(t[tail + 3][base_row + u]);
 
@@ -609,12 +650,47 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
       lin3(bt[16], d, 4 * d, sc + 4);                     // mlp.2
       lin3(bt[2], 3 * d, d, sc + 5);                      // attn_s.qkv
     }
+    // head (last tubelet frame rows, model.py:119-120) in 4 chunks of 4 patch
+    // rows = 64c columns: the last-block kernel streams one chunk at a time
+    const float* hw3 = t[tail + 2];
+    const size_t hrow0 = size_t(T - 1) * p * p * c;
+    auto head_at = [&](int n, int k) { return hw3[(hrow0 + n) * d + k]; };
+    const int sh = exponent_for(maxabs(D.used, d, head_at));
+    m->W.tc.sc_head = std::ldexp(1.f, -sh);
+    size_t head3_off = 0;
+    const int hchunk = D.used / 4;
+    for (int j = 0; j < 4; ++j) {
+      const size_t o = pack2(hchunk, d, [&](int n, int k) { return head_at(hchunk * j + n, k); }, sh);
+      if (j == 0) head3_off = o;
+    }
+    // the last block re-packed as the streaming chunks of k_last_tc.cu (each a
+    // contiguous [hi | lo] block <= 48 KB): proj_s, qkv_t, proj_t, fc1 rows
+    // 0-127 / 128-255, fc2 K 0-127 / 128-255 (same exponents as blk3)
+    size_t last3_off = 0;
+    {
+      const int li = D.layers - 1;
+      const float* const* bt = t + 3 + 18 * li;
+      const float* sc = m->W.tc.sc_blk[li];
+      auto ex = [](float scv) { return -int(std::lround(std::log2(double(scv)))); };
+      auto mat = [&](const float* wt, int K, int n0, int k0) {
+        return [=](int n, int k) { return wt[size_t(n0 + n) * K + k0 + k]; };
+      };
+      last3_off = pack2(d, d, mat(bt[4], d, 0, 0), ex(sc[0]));             // proj_s
+      pack2(3 * d, d, mat(bt[8], d, 0, 0), ex(sc[1]));                      // qkv_t
+      pack2(d, d, mat(bt[10], d, 0, 0), ex(sc[2]));                         // proj_t
+      pack2(2 * d, d, mat(bt[14], d, 0, 0), ex(sc[3]));                     // fc1 rows 0..127
+      pack2(2 * d, d, mat(bt[14], d, 2 * d, 0), ex(sc[3]));                 // fc1 rows 128..255
+      pack2(d, 2 * d, mat(bt[16], 4 * d, 0, 0), ex(sc[4]));                 // fc2 K 0..127
+      pack2(d, 2 * d, mat(bt[16], 4 * d, 0, 2 * d), ex(sc[4]));             // fc2 K 128..255
+    }
     CK(cudaMalloc(&m->blob_x3, h3.size() * sizeof(__half)), "cudaMalloc(x3)");
     CK(cudaMemcpy(m->blob_x3, h3.data(), h3.size() * sizeof(__half), cudaMemcpyHostToDevice),
        "cudaMemcpy(x3)");
     m->W.tc.emb3 = m->blob_x3 + emb3_off;
     m->W.tc.qkv0_3 = m->blob_x3 + q3off;
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk3[i] = m->blob_x3 + blk3[i];
+    m->W.tc.head3 = m->blob_x3 + head3_off;
+    m->W.tc.last3 = m->blob_x3 + last3_off;
   }
   m->loaded = true;
   return 0;
@@ -889,6 +965,7 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
 #ifdef NVREC_TRACE
 // trace build only (not in include/nvrec_b200.h): phase timestamps of one CTA
 int nvrec_debug_attn_trace(unsigned long long* host, int n) { return nvrec::attn_trace(host, n); }
+int nvrec_debug_last_trace(unsigned long long* host, int n) { return nvrec::last_trace(host, n); }
 #endif
 
 int64_t nvrec_attn_fixup_items(void) {

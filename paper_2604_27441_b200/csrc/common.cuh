@@ -115,6 +115,14 @@ struct TcW {
   const __half* emb3;           // [T*16/kPy stages][hi 64 x 16 kPy c | lo ...], kPy = 2 (RGB) / 4
   const __half* qkv0_3;         // [hi 192x64 | lo 192x64] block-0 qkv_s
   const __half* blk3[8];        // per block: proj_s | qkv_t | proj_t | fc1 | fc2 | qkv_s, each [hi | lo]
+  // head rows of the last tubelet frame in 4 chunks of 4 patch rows (64c
+  // columns), each [hi 64c x 64 | lo 64c x 64] (k_last_tc.cu)
+  const __half* head3;
+  float sc_head;
+  // the last block's matrices as k_last_tc.cu streams them: proj_s | qkv_t |
+  // proj_t | fc1 rows 0-127 | fc1 rows 128-255 | fc2 K 0-127 | fc2 K 128-255,
+  // each [hi | lo] (scales sc_blk[layers - 1])
+  const __half* last3;
   float sc_emb, sc_qkv0;
   float sc_blk[8][6];
 };

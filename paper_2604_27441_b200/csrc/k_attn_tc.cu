@@ -959,15 +959,24 @@ attn_combine_kernel(const float* __restrict__ part, float* __restrict__ ao,
   const int it = (seq / heads) % nt, hh = seq % heads;
   const int e = threadIdx.x & 31;
   for (int q = blockIdx.x * 8 + (threadIdx.x >> 5); q < nq; q += gridDim.x * 8) {
+    // every split's loads in flight at once: unrolled to the maximum split
+    // count, splits past `splits` re-read the last one with weight 0
+    float ms[kAttnMaxSplits], ls[kAttnMaxSplits], os[kAttnMaxSplits];
     float M = -INFINITY;
-    for (int sp = 0; sp < splits; ++sp)
-      M = fmaxf(M, __ldg(part + ((size_t(sp) * seqs + seq) * ns + q) * kPart + 32));
+#pragma unroll
+    for (int sp = 0; sp < kAttnMaxSplits; ++sp) {
+      const float* p = part + ((size_t(min(sp, splits - 1)) * seqs + seq) * ns + q) * kPart;
+      ms[sp] = __ldg(p + 32);
+      ls[sp] = __ldg(p + 33);
+      os[sp] = __ldg(p + e);
+      M = fmaxf(M, ms[sp]);
+    }
     float o = 0.f, L = 0.f;
-    for (int sp = 0; sp < splits; ++sp) {
-      const float* p = part + ((size_t(sp) * seqs + seq) * ns + q) * kPart;
-      const float w = ex2(__ldg(p + 32) - M);
-      L = fmaf(__ldg(p + 33), w, L);
-      o = fmaf(__ldg(p + e), w, o);
+#pragma unroll
+    for (int sp = 0; sp < kAttnMaxSplits; ++sp) {
+      const float w = sp < splits ? ex2(ms[sp] - M) : 0.f;
+      L = fmaf(ls[sp], w, L);
+      o = fmaf(os[sp], w, o);
     }
     const size_t off = (size_t(b * nt + it) * ns + q) * d + hh * kHd + e;
     if (ao_half) reinterpret_cast<__half*>(ao)[off] = __float2half_rn(o / L);
@@ -1149,7 +1158,9 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
   if (n_kernels) *n_kernels = (mode == 1 || !A.redo_list ? 1 : 2) + (combine ? 1 : 0);
   if (splits_out) *splits_out = ta.splits;
   if (combine) {
-    dim3 cg(ceil_div(count ? 128 : A.ns, 8), seqs);
+    // pruned launches: the compact row count is on the device; size for up to
+    // 512 rows per sequence per pass (rows past the count exit at once)
+    dim3 cg(ceil_div(count ? (A.ns < 512 ? A.ns : 512) : A.ns, 8), seqs);
     launch_pdl(attn_combine_kernel, cg, 256, 0, s, A.part, A.ao, count, seqs, ta.splits, D.nt,
                D.heads, A.ns, D.d, int(ao_half));
   }

@@ -116,6 +116,33 @@ struct TokenX3Args {
 };
 cudaError_t launch_token_x3(const TokenX3Args& a, cudaStream_t s);
 
+// tensor-core LAST block + final LayerNorm + head on the masked patches
+// (k_last_tc.cu); split-fp16 (fp32-class) products on both precision paths
+struct LastTcArgs {
+  int b, ns, nt, c;             // streams, positions per slice, time slices, channels
+  int img_h, img_w, nw;
+  const int* list;              // [b][ns] masked positions (ascending), or null = all
+  const int* count;             // [b] entries of list, or null
+  const float* x;               // [b][nt][ns][64] residual stream (positions)
+  const float* ao;              // [b][nt][ns][64] attention output, row r <-> list[r]
+  const __half* w_blk;          // the last block's streaming pack (TcW::last3)
+  const __half* w_head;         // TcW::head3
+  float sc[5];                  // 2^-s: proj_s, qkv_t, proj_t, fc1, fc2
+  float sc_head;
+  const float *b_proj_s, *ln_t_w, *ln_t_b, *b_qkv_t, *b_proj_t, *ln_m_w, *ln_m_b;
+  const float *b_fc1, *b_fc2, *norm_w, *norm_b, *head_b;
+  float* out_f32;               // (b, c, h, w) or null
+  uint8_t* out_u8;              // (b, h, w, c) or null
+  uint8_t* out_frames;          // or: in place into stream b's corrupted plane,
+  const int32_t* out_slot;      //   frames + out_slot[b * slot_stride] * frame_bytes
+  int slot_stride;
+  size_t frame_bytes;
+  int max_hsplit;                // CTAs that may share a tile (1, 2 or 4)
+};
+bool last_tc_supported(const Dims& D, int b);
+// grid_rows: an upper bound of the gathered rows (sizes the grid)
+cudaError_t launch_last_tc(const LastTcArgs& a, int grid_rows, cudaStream_t s);
+
 cudaError_t launch_embed(const EmbedArgs& a, bool u8, int b, cudaStream_t s);
 cudaError_t launch_ln_qkv(const LnQkvArgs& a, int b, cudaStream_t s);
 cudaError_t launch_copy_plane(const uint8_t* frames, const int32_t* frame_index, int F,
@@ -132,6 +159,7 @@ cudaError_t launch_attn_tc(const Act& A, const Dims& D, const int* count, cudaSt
 int64_t attn_fixup_items();   // -1 on a CUDA error
 #ifdef NVREC_TRACE
 int attn_trace(unsigned long long* host, int n);   // trace build (tools/trace_attn.py)
+int last_trace(unsigned long long* host, int n);   // trace build (tools/trace_last.py)
 #endif
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,

@@ -92,6 +92,16 @@ class MaskedVideoModel(nn.Module):
                 self._packed_sig = sig
             return self._native
 
+    def native_snapshot(self, device=None) -> _native.NativeModel:
+        """A private packed copy of the current weights.  Serving pipelines
+        capture CUDA graphs over the packed weight pointers, so they must not
+        share the re-packable ``native()`` object: a later ``load_state_dict``
+        followed by a module call would free the blob their graphs read."""
+        dev = _native.require_cuda(device)
+        nat = _native.NativeModel(self.config, self.channels, dev)
+        nat.load(list(self.state_dict().values()))
+        return nat
+
     # -- forward -------------------------------------------------------------
 
     def forward(self, stack: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:

@@ -71,7 +71,7 @@ class ReceiverPipeline:
         # the step's slot table rides in with its inputs, so one CUDA graph
         # (decode + recovery) per buffer set serves every ring phase
         self.tab_cur = torch.empty((nbuf, n, self.F), dtype=torch.int32, device=dev)
-        self.nat = engine.model.native(dev)          # weights snapshotted
+        self.nat = engine.model.native_snapshot(dev)  # private weight snapshot
         self.use_graphs = graphs
         self._graphs = {}
         self.s_h2d = torch.cuda.Stream(dev)

@@ -163,9 +163,10 @@ class RecoveryPipeline:
         # per buffer set: the step's slot table, copied in with its inputs, so
         # one CUDA graph per buffer set serves every ring phase
         self.tab_cur = torch.empty((nbuf, n, self.F), dtype=torch.int32, device=dev)
-        # the weights are snapshotted for the pipeline's lifetime (re-create
-        # it after loading new weights)
-        self.nat = engine.model.native(dev)
+        # a private weight snapshot for the pipeline's lifetime: its CUDA
+        # graphs hold the packed weight pointers (re-create the pipeline to
+        # serve new weights)
+        self.nat = engine.model.native_snapshot(dev)
         self.s_h2d = torch.cuda.Stream(dev)
         # one DMA stream reaches ~40 GB/s host->device; four in parallel ~51
         self.s_parts = [torch.cuda.Stream(dev) for _ in range(max(1, min(h2d_streams, n)))]

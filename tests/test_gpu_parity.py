@@ -217,18 +217,22 @@ def test_fast_path_runs_tensor_core_attention():
     with _native.StageProfile() as prof:
         m(s, mk)
         torch.cuda.synchronize()
-    # two blocks x (tcgen05 attention + its exact fix-up launch)
+    # two blocks x (tcgen05 attention + its exact fix-up launch), the last
+    # block + head on tcgen05 (k_last_tc.cu)
     assert prof.launches["attn_tc"] == 4 and prof.launches["attn_simt"] == 0
+    assert prof.launches["last_tc"] == 1
     m.precision = "precise"
     with _native.StageProfile() as prof:
         m(s, mk)
         torch.cuda.synchronize()
     assert prof.launches["attn_tc"] == 4 and prof.launches["attn_simt"] == 0
+    assert prof.launches["last_tc"] == 1
     small = p.MaskedVideoModel(p.ModelConfig(dim=16, heads=2), 3, precision="precise")
     with _native.StageProfile() as prof:
         small(s, mk)
         torch.cuda.synchronize()
     assert prof.launches["attn_simt"] == 2 and prof.launches["attn_tc"] == 0
+    assert prof.launches["last_tc"] == 0
 
 
 def test_fast_vs_reference_error_budget_720p():
@@ -281,3 +285,49 @@ def test_speculative_max_matches_exact_maxima(tmp_path, precision):
     # the sharp case overflows the speculative exponent: the exact fix-up
     # (a multi-CTA list walk) must have redone work items
     assert int(spec["redone"]) > 0
+
+
+def test_last_block_tc_equals_simt(tmp_path):
+    """The tcgen05 last block + head (rows gathered across streams, 32..128
+    per tile, split-fp16 products) against the fp32 CUDA-core last block
+    (NVREC_LAST_SIMT=1) on the same inputs: u8 within 1 LSB, float outputs
+    within 2e-6; streams with no or all patches masked included."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    res = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / ("l%s.npz" % flag))
+        subprocess.run([sys.executable, os.path.join(here, "last_block_probe.py"), path],
+                       check=True, env=dict(os.environ, NVREC_LAST_SIMT=flag), timeout=300)
+        res[flag] = np.load(path)
+    tc, simt = res["0"], res["1"]
+    for c in (3, 1):
+        for prec in ("fast", "precise"):
+            key = "%d_%s" % (c, prec)
+            assert int(tc["last_tc_" + key]) == 1 and int(simt["last_tc_" + key]) == 0
+            d = np.abs(tc["u8_" + key].astype(int) - simt["u8_" + key].astype(int))
+            assert d.max() <= 1, (key, d.max())
+            e = np.abs(tc["f32_" + key] - simt["f32_" + key]).max()
+            assert e <= 2e-6, (key, e)
+
+
+@pytest.mark.parametrize("c", [3, 1])
+def test_recover_720p_20pct_vs_oracle(c):
+    """1280x720 at 20 % block loss (the density where the last block used to
+    dominate): both precisions vs the CPU oracle, u8 LSB and SSIM bars."""
+    from paper_2604_27441_b200.recovery import RecoveryEngine
+    arch = nvrec_forward.Arch()
+    rng = np.random.default_rng(7200 + c)
+    state = make_state(arch, c, 72000 + c)
+    frames = textured_u8(rng, 6, 720, 1280, c)
+    grid = block_grid(rng, 45, 80, 0.2)
+    plane = frames[-1].copy()
+    want = oracle_recover.recover(state, arch, c, plane, grid, list(frames[:-1]))
+    for prec in ("fast", "precise"):
+        eng = RecoveryEngine(_model(arch, c, state, prec), prec)
+        got = eng.recover(plane, grid, list(frames[:-1]))
+        d = np.abs(got.astype(int) - want.astype(int))
+        assert d.max() <= LSB[prec], (prec, d.max())
+        ds = abs(ssim(frames[-1], got) - ssim(frames[-1], want))
+        assert ds <= SSIM_TOL, (prec, ds)
