@@ -57,6 +57,15 @@ namespace {
 
 using namespace sm100;
 
+// End-of-group rendezvous of the role-split loops (TMA/MMA warps and softmax
+// warps run separate loops over the same work items, so the CTA meets at two
+// different barrier instructions): the NON-aligned form, which PTX allows to
+// be reached from different code locations (__syncthreads / bar.sync are
+// .aligned: one instruction for the whole CTA).
+__device__ __forceinline__ void group_barrier() {
+  asm volatile("barrier.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+}
+
 constexpr int kHd = 32;
 constexpr int kTileQ = 128;
 constexpr int kTileK = 128;
@@ -361,7 +370,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
     tc_fence_before();
     __syncwarp();
-    __syncthreads();
+    group_barrier();
     tc_fence_after();
     if (!kExact && warp == kProducer && lane == 0 && sm.redo[gq_done % 3] != 0) {
       const int idx = atomicAdd(a.redo_list, 1);     // overflowed: exact fix-up later
@@ -632,7 +641,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
     tc_fence_before();
     __syncwarp();
-    __syncthreads();
+    group_barrier();
     tc_fence_after();
     (void)gq_done;
   }
