@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define NVREC_ABI_VERSION 4
+#define NVREC_ABI_VERSION 5
 
 enum {
   NVREC_OK = 0,
@@ -117,6 +117,20 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
                      const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
                      const uint8_t* mask_bits, uint8_t* out, void* workspace,
                      int64_t workspace_bytes, int32_t precision, void* stream);
+
+/* 16-bit depth extension of nvrec_recover_u8 (the reference's wire format is
+ * u8 only; SPEC.md:74 names 16-bit depth an extension point): frames are u16
+ * planes (h, w) of a channels == 1 model at `frames + slot * h*w` (elements),
+ * normalised as u16 / 65535 and quantised as clip(out * 65535 + 0.5, 0,
+ * 65535) -- the u8 rule of server.py:189-194 at 16 bits -- then merged through
+ * the block mask.  Same slot table, mask bits, aliasing and in-place (out ==
+ * NULL) rules as nvrec_recover_u8.  Needs the tensor-core envelope
+ * (dim 64, 2 heads, patch 16, stack slices <= 3): NVREC_E_UNSUPPORTED
+ * otherwise. */
+int nvrec_recover_u16(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                      const uint16_t* frames, int32_t n_slots, const int32_t* frame_index,
+                      const uint8_t* mask_bits, uint16_t* out, void* workspace,
+                      int64_t workspace_bytes, int32_t precision, void* stream);
 
 /* One P-frame's loss-mask job (all pointers are DEVICE pointers). */
 typedef struct nvrec_lossmask_job {

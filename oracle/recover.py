@@ -51,6 +51,22 @@ def recover(state: dict | None, arch: nvrec_forward.Arch, channels: int,
     return np.where(pix[:, :, None], pred, plane)                 # :196
 
 
+def recover16(state: dict | None, arch: nvrec_forward.Arch, plane: np.ndarray,
+              grid: np.ndarray, refs: list[np.ndarray]) -> np.ndarray:
+    """16-bit depth extension of server.py:181-196 (SPEC.md:74 names 16-bit
+    depth an extension point; the wire format is u8): the same stack / mask /
+    forward / merge with 65535 in place of 255.  ``plane``/``refs`` are u16
+    (h, w); returns the merged u16 (h, w)."""
+    pix = grid_to_pixels(grid)
+    if state is None or not refs or not pix.any():
+        return np.ascontiguousarray(plane)
+    stack_np = np.stack(list(refs[-arch.k:]) + [plane]).astype(np.float32) / 65535.0
+    stack = torch.from_numpy(stack_np)[None, :, None]
+    out = nvrec_forward.forward(state, arch, 1, stack, torch.from_numpy(pix)[None]).numpy()[0, 0]
+    pred = np.clip(out * 65535.0 + 0.5, 0, 65535).astype(np.uint16)
+    return np.where(pix, pred, plane)
+
+
 def masked_merge(original: np.ndarray, recovered: np.ndarray,
                  grid: np.ndarray) -> np.ndarray:
     """recovery.py:86-91 (client-side re-merge)."""

@@ -28,13 +28,13 @@ E_INVALID, E_UNSUPPORTED, E_CUDA, E_WORKSPACE, E_STATE = -1, -2, -3, -4, -5
 
 EXPORTS = ("nvrec_abi_version", "nvrec_last_error", "nvrec_model_create",
            "nvrec_model_destroy", "nvrec_model_load", "nvrec_workspace_bytes",
-           "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_loss_mask",
+           "nvrec_forward_f32", "nvrec_recover_u8", "nvrec_recover_u16", "nvrec_loss_mask",
            "nvrec_profile_begin", "nvrec_profile_end", "nvrec_baseline_workspace_bytes",
            "nvrec_baseline_u8", "nvrec_decode", "nvrec_rs_plan", "nvrec_rs_reconstruct",
            "nvrec_attn_fixup_items")
 STAGES = ("lossmask", "masklist", "copy", "embed", "ln_qkv", "attn_simt", "attn_tc",
           "token", "baseline", "decode", "rs", "last_tc")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class NativeError(RuntimeError):
@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.nvrec_forward_f32.argtypes = [vp, vp, i32, i32, i32, i32, i32, vp, vp,
                                           vp, i64, i32, vp]
         lib.nvrec_recover_u8.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp, vp,
+                                         i64, i32, vp]
+        lib.nvrec_recover_u16.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp, vp,
                                          i64, i32, vp]
         lib.nvrec_loss_mask.argtypes = [vp, i32, vp]
         lib.nvrec_baseline_workspace_bytes.argtypes = [i32, i32, i32, i32]
@@ -215,6 +217,19 @@ class NativeModel:
                                         frames.shape[0], frame_index.data_ptr(), mask_bits.data_ptr(),
                                         None if out is None else out.data_ptr(),
                                         ws.data_ptr(), ws.numel(), prec, stream_ptr()))
+        return out
+
+
+    def recover_u16(self, frames: torch.Tensor, frame_index: torch.Tensor,
+                    mask_bits: torch.Tensor, out: torch.Tensor | None, b: int, h: int, w: int,
+                    prec: int) -> torch.Tensor | None:
+        """16-bit depth planes (n_slots, h, w) uint16; out=None merges in place."""
+        ws = self.workspace(b, h, w, prec)
+        check(self.lib.nvrec_recover_u16(self.handle, b, h, w, frames.data_ptr(),
+                                         frames.shape[0], frame_index.data_ptr(),
+                                         mask_bits.data_ptr(),
+                                         None if out is None else out.data_ptr(),
+                                         ws.data_ptr(), ws.numel(), prec, stream_ptr()))
         return out
 
 

@@ -272,7 +272,7 @@ struct InPlace {
 
 int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, int am,
                bool pruned, int h, int w, float* out_f32, uint8_t* out_u8,
-               cudaStream_t s, InPlace ip = {}) {
+               cudaStream_t s, InPlace ip = {}, bool u16 = false) {
   const Dims& D = m->D;
   const int b = A.b;
   const bool fast = am == 1;
@@ -338,7 +338,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
     ta.out_frames = ip.frames;
     ta.out_slot = ip.frame_index ? ip.frame_index + (D.F - 1) : nullptr;
     ta.slot_stride = D.F;
-    ta.frame_bytes = size_t(h) * w * D.c;
+    ta.frame_bytes = size_t(h) * w * D.c * (u16 ? 2 : 1);
     if (last_tc) {
       const nvrec::BlockW& bw = m->W.blk[li];
       nvrec::LastTcArgs la{};
@@ -358,6 +358,7 @@ int run_blocks(const nvrec_model* m, nvrec::Act& A, const WorkspaceLayout& L, in
       la.out_f32 = out_f32; la.out_u8 = out_u8;
       la.out_frames = ip.frames; la.out_slot = ta.out_slot;
       la.slot_stride = D.F; la.frame_bytes = ta.frame_bytes;
+      la.u16 = u16;
       static const int hs_env = [] {
         const char* e = getenv("NVREC_LAST_HSPLIT");   // A/B: CTAs per tile cap
         return e ? atoi(e) : 4;
@@ -575,6 +576,20 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
       lin(bt[16], d, 4 * d);                           // mlp.2
       lin(bt[2], 3 * d, d);                            // attn_s.qkv
     }
+    // 16-bit depth embedding (k_embed_tc.cu, C == 2): per 2-patch-row stage,
+    // K = (py, px, byte), byte 0 = lo (W), byte 1 = hi (256 W)
+    auto at16 = [&](int tt, int py0) {
+      return [&, tt, py0](int n, int k) {
+        const int pyl = k / 32, rem = k % 32, px = rem / 2;
+        return ew_at(n, 0, tt, py0 + pyl, px) * ((rem & 1) ? 256.f : 1.f);
+      };
+    };
+    size_t emb16_off = SIZE_MAX;
+    if (c == 1)
+      for (int st = 0; st < T * 8; ++st) {
+        const size_t o = pack(d, 64, at16(st / 8, 2 * (st % 8)));
+        if (st == 0) emb16_off = o;
+      }
     CK(cudaMalloc(&m->blob_bf16, hb.size() * sizeof(__half)), "cudaMalloc(fp16)");
     CK(cudaMemcpy(m->blob_bf16, hb.data(), hb.size() * sizeof(__half),
                   cudaMemcpyHostToDevice), "cudaMemcpy(fp16)");
@@ -582,6 +597,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     m->W.tc.emb_stage_elems = d * kst;
     m->W.tc.qkv0 = m->blob_bf16 + qoff;
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk[i] = m->blob_bf16 + blk_pack[i];
+    m->W.tc.emb16 = emb16_off == SIZE_MAX ? nullptr : m->blob_bf16 + emb16_off;
 
     // ---- split-fp16 [hi | lo] packs for the precise path ----------------------
     // W * 2^s with max|W| 2^s in [2^13, 2^14): hi = fp16(W 2^s) and lo =
@@ -650,6 +666,16 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
       lin3(bt[16], d, 4 * d, sc + 4);                     // mlp.2
       lin3(bt[2], 3 * d, d, sc + 5);                      // attn_s.qkv
     }
+    // 16-bit depth embedding, split: one exponent for lo and hi (x 256) bytes
+    size_t emb16_3_off = SIZE_MAX;
+    if (c == 1) {
+      const int s16 = exponent_for(256.f * emx);
+      m->W.tc.sc_emb16 = std::ldexp(1.f, -s16);
+      for (int st = 0; st < T * 8; ++st) {
+        const size_t o = pack2(d, 64, at16(st / 8, 2 * (st % 8)), s16);
+        if (st == 0) emb16_3_off = o;
+      }
+    }
     // head (last tubelet frame rows, model.py:119-120) in 4 chunks of 4 patch
     // rows = 64c columns: the last-block kernel streams one chunk at a time
     const float* hw3 = t[tail + 2];
@@ -690,6 +716,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     m->W.tc.qkv0_3 = m->blob_x3 + q3off;
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk3[i] = m->blob_x3 + blk3[i];
     m->W.tc.head3 = m->blob_x3 + head3_off;
+    m->W.tc.emb16_3 = emb16_3_off == SIZE_MAX ? nullptr : m->blob_x3 + emb16_3_off;
     m->W.tc.last3 = m->blob_x3 + last3_off;
   }
   m->loaded = true;
@@ -803,10 +830,11 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b, int32
   return run_blocks(m, A, L, am, false, h, w, out, nullptr, s);
 }
 
-int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
-                     const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
-                     const uint8_t* mask_bits, uint8_t* out, void* ws, int64_t ws_bytes,
-                     int32_t precision, void* stream) {
+// u8 planes (nvrec_recover_u8) or u16 depth planes (nvrec_recover_u16)
+static int recover_planes(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                          const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
+                          const uint8_t* mask_bits, uint8_t* out, void* ws, int64_t ws_bytes,
+                          int32_t precision, void* stream, bool u16) {
   WorkspaceLayout L;
   int rc = common_checks(m, b, h, w, ws, ws_bytes, precision, &L);
   if (rc) return rc;
@@ -818,6 +846,11 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   nvrec::Act A = make_act(m, ws, L, b, h, w);
   const int am = attn_mode(m->D, precision);
+  if (u16 && (m->D.c != 1 || am == 0 || !nvrec::embed_tc_supported(m->D) ||
+              !m->W.tc.emb16 || !m->W.tc.emb16_3 || !m->W.tc.last3 || precise_simt() ||
+              last_simt() || !nvrec::last_tc_supported(m->D, b)))
+    return fail(NVREC_E_UNSUPPORTED, "u16 depth path needs a channels == 1 model inside the "
+                "tensor-core envelope (dim 64, 2 heads, patch 16, <= 3 time slices)");
   const bool fast = am == 1;
   const int nbytes = (A.ns + 7) / 8;
   cudaError_t e;
@@ -829,6 +862,7 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
   if (am && nvrec::embed_tc_supported(m->D) && (am == 1 || !precise_simt())) {
     nvrec::EmbedTcArgs ea{};
     ea.x3 = am == 2;
+    ea.u16 = u16;
     ea.D = m->D;
     ea.tcw = &m->W.tc;
     ea.emb_wmsum = m->W.emb_wmsum; ea.emb_b = m->W.emb_b; ea.time_pos = m->W.time_pos;
@@ -840,7 +874,8 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
     ea.x = A.x; ea.qh = A.qh; ea.kh = A.kh; ea.vth = A.vth;
     // the embedding output goes to block 0's tensor-core tail in fp16 (half
     // the traffic of that one hand-off; the tail keeps the residual in fp32)
-    A.x_half = fast && A.xh && m->D.layers > 1 && nvrec::token_tc_supported(m->D) && m->W.tc.blk[0];
+    A.x_half = fast && !u16 && A.xh && m->D.layers > 1 && nvrec::token_tc_supported(m->D) &&
+               m->W.tc.blk[0];
     ea.xh = A.x_half ? A.xh : nullptr;
     ea.b = b; ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns; ea.ns_pad = A.ns_pad;
     cudaError_t e2;
@@ -854,23 +889,41 @@ int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
                         precision, s);
     if (rc) return rc;
   }
+  const size_t frame_bytes = size_t(h) * w * m->D.c * (u16 ? 2 : 1);
   if (!out) {
     // in place: the corrupted plane already holds every trusted pixel; only
     // the masked patches are written (after the embedding read the stack)
     InPlace ip;
     ip.frames = const_cast<uint8_t*>(frames);
     ip.frame_index = frame_index;
-    return run_blocks(m, A, L, am, true, h, w, nullptr, nullptr, s, ip);
+    return run_blocks(m, A, L, am, true, h, w, nullptr, nullptr, s, ip, u16);
   }
   // the merge base (corrupted plane) is copied only after the embedding has
   // read every stacked frame, so `out` may alias a reference slot (a ring
   // that takes the recovered plane in place of its oldest reference)
   {
     ProfScope ps(NVREC_STAGE_COPY, s);
-    e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, size_t(h) * w * m->D.c, out, b, s);
+    e = nvrec::launch_copy_plane(frames, frame_index, m->D.F, frame_bytes, out, b, s);
   }
   if (e != cudaSuccess) return cuda_fail(e, "copy launch");
-  return run_blocks(m, A, L, am, true, h, w, nullptr, out, s);
+  return run_blocks(m, A, L, am, true, h, w, nullptr, out, s, {}, u16);
+}
+
+int nvrec_recover_u8(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                     const uint8_t* frames, int32_t n_slots, const int32_t* frame_index,
+                     const uint8_t* mask_bits, uint8_t* out, void* ws, int64_t ws_bytes,
+                     int32_t precision, void* stream) {
+  return recover_planes(m, b, h, w, frames, n_slots, frame_index, mask_bits, out, ws, ws_bytes,
+                        precision, stream, false);
+}
+
+int nvrec_recover_u16(const nvrec_model* m, int32_t b, int32_t h, int32_t w,
+                      const uint16_t* frames, int32_t n_slots, const int32_t* frame_index,
+                      const uint8_t* mask_bits, uint16_t* out, void* ws, int64_t ws_bytes,
+                      int32_t precision, void* stream) {
+  return recover_planes(m, b, h, w, reinterpret_cast<const uint8_t*>(frames), n_slots,
+                        frame_index, mask_bits, reinterpret_cast<uint8_t*>(out), ws, ws_bytes,
+                        precision, stream, true);
 }
 
 int nvrec_loss_mask(const nvrec_lossmask_job* jobs, int32_t n_jobs, void* stream) {

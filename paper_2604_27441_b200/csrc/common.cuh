@@ -119,6 +119,12 @@ struct TcW {
   // columns), each [hi 64c x 64 | lo 64c x 64] (k_last_tc.cu)
   const __half* head3;
   float sc_head;
+  // 16-bit depth embedding (channels == 1): per 2-patch-row stage the K axis is
+  // (py, px, byte) with byte 0 = lo (W) and byte 1 = hi (256 W); fp16 packs
+  // (emb16) and [hi | lo] split packs scaled by 2^s16 (emb16_3, sc = 2^-s16)
+  const __half* emb16;
+  const __half* emb16_3;
+  float sc_emb16;
   // the last block's matrices as k_last_tc.cu streams them: proj_s | qkv_t |
   // proj_t | fc1 rows 0-127 | fc1 rows 128-255 | fc2 K 0-127 | fc2 K 128-255,
   // each [hi | lo] (scales sc_blk[layers - 1])

@@ -27,6 +27,11 @@
 // y = y_hi + y_lo and the qkv GEMM is y_hi W_hi + y_hi W_lo + y_lo W_hi.  x
 // leaves in fp32; q/k/v leave as bf16 hi/lo pairs in the split attention
 // layouts (QkvDst::x3).  One CTA per SM (the doubled rings take ~135 KB).
+//
+// 16-bit depth (nvrec_recover_u16): C == 2 reads each u16 pixel as its two
+// bytes (lo, hi) -- exact in fp16 like u8 pixels -- against weights W (lo) and
+// 256 W (hi) (TcW::emb16 / emb16_3), and the epilogue divides by 65535: the
+// same GEMM as W . (u16 / 65535), with no conversion pass over the planes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -52,13 +57,13 @@ constexpr int kThreads = 192;
 template <int C, bool X3 = false>
 struct __align__(128) EmbSmem {
   static constexpr int kX = X3 ? 2 : 1;                      // hi (+ lo) operand copies
-  static constexpr int kPy = C == 3 ? 2 : 4;                 // patch rows per K stage
+  static constexpr int kPy = C == 1 ? 4 : 2;                 // patch rows per K stage
   static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame
   // A/W (MMA operand) ring: 2 stages for both modalities (a 3-stage depth
   // ring measured the same 79.6 us per 8 x 720p launch and trips
   // compute-sanitizer synccheck's mbarrier tracking)
   static constexpr int kNst = 2;
-  static constexpr int kNu8 = C == 3 ? 3 : 4;                // raw-pixel TMA ring
+  static constexpr int kNu8 = C == 1 ? 4 : 3;                // raw-pixel TMA ring
   static constexpr uint32_t kU8 = kTh * kPy * kTw * 16 * C; // raw pixels per stage
   static constexpr uint32_t kA = kRows * 16 * kPy * C * 2;  // fp16 A per stage
   static constexpr uint32_t kW1 = 64 * 16 * kPy * C * 2;    // fp16 W per stage (one copy)
@@ -164,8 +169,10 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         mbar_expect_tx(&sm.w_full[ps], S::kW);
         // the host packs 2-row stages back to back, so kPy/2 of them are one
         // block (X3: one [hi | lo] pair per kernel stage)
-        const __half* src = X3 ? tcw.emb3 + size_t(st) * (S::kW / 2)
-                               : tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems;
+        const __half* src =
+            C == 2 ? (X3 ? tcw.emb16_3 + size_t(st) * (S::kW / 2) : tcw.emb16 + size_t(st) * (S::kW / 2))
+                   : (X3 ? tcw.emb3 + size_t(st) * (S::kW / 2)
+                         : tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems);
         bulk_load(sm.w[ps], src, S::kW, &sm.w_full[ps]);
       }
       // qkv weights into the A ring once the last embed MMA has read it
@@ -264,8 +271,10 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       }
     }
     const bool mterm = last_slice && masked;
-    // (X3: the weights were scaled by 2^s; 2^-s / 255 is exactly 2^-s fl(1/255))
-    const float inv255 = X3 ? tcw.sc_emb * (1.f / 255.f) : 1.f / 255.f;
+    // (X3: the weights were scaled by 2^s; 2^-s / 255 is exactly 2^-s fl(1/255));
+    // u16 depth (C == 2: byte pairs, hi-byte weights x 256) is / 65535
+    const float pix_inv = C == 2 ? 1.f / 65535.f : 1.f / 255.f;
+    const float inv255 = X3 ? (C == 2 ? tcw.sc_emb16 : tcw.sc_emb) * pix_inv : pix_inv;
 #pragma unroll
     for (int o = 0; o < 64; ++o) {
       float v = fmaf(x[o], inv255, sm.par[o]);
@@ -424,6 +433,9 @@ bool embed_tc_supported(const Dims& D) {
 }
 
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s) {
+  // 16-bit depth: the u16 plane is read as byte pairs (lo, hi), i.e. a
+  // two-"channel" u8 image whose hi-byte weights carry the factor 256
+  if (a.u16) return a.x3 ? launch_c<2, true>(a, s) : launch_c<2, false>(a, s);
   if (a.x3) return a.D.c == 3 ? launch_c<3, true>(a, s) : launch_c<1, true>(a, s);
   return a.D.c == 3 ? launch_c<3, false>(a, s) : launch_c<1, false>(a, s);
 }

@@ -539,8 +539,9 @@ last_tc_kernel(LastTcArgs a) {
     if (t0) issue_head(0);
     const int ih = s / a.nw, iw = s - (s / a.nw) * a.nw;
     uint8_t* ob = nullptr;
+    const int pix_bytes = a.u16 ? 2 * c : c;                      // u16 depth: 2 bytes
     if (valid && !a.out_f32)
-      ob = a.out_u8 ? a.out_u8 + size_t(b) * a.img_h * a.img_w * c
+      ob = a.out_u8 ? a.out_u8 + size_t(b) * a.img_h * a.img_w * pix_bytes
                     : a.out_frames + size_t(a.out_slot[b * a.slot_stride]) * a.frame_bytes;
 #pragma unroll 1
     for (int i = 0; i < nh; ++i) {
@@ -585,6 +586,21 @@ last_tc_kernel(LastTcArgs a) {
             const int px = (q * 16 + e) / c, ch = (q * 16 + e) - px * c;
             a.out_f32[((size_t(b) * c + ch) * a.img_h + yy) * a.img_w + iw * 16 + px] = sg[e];
           }
+        } else if (C == 1 && a.u16) {
+          // np.clip(out * 65535.0 + 0.5, 0, 65535).astype(np.uint16) (16-bit
+          // depth, the u8 rule at 16 bits): f32 mul, f32 add, truncate
+          uint32_t wd[8];
+#pragma unroll
+          for (int e2 = 0; e2 < 8; ++e2) {
+            float q0 = __fadd_rn(__fmul_rn(sg[2 * e2], 65535.f), 0.5f);
+            float q1 = __fadd_rn(__fmul_rn(sg[2 * e2 + 1], 65535.f), 0.5f);
+            q0 = fminf(fmaxf(q0, 0.f), 65535.f);
+            q1 = fminf(fmaxf(q1, 0.f), 65535.f);
+            wd[e2] = uint32_t(q0) | (uint32_t(q1) << 16);
+          }
+          uint4* o16 = reinterpret_cast<uint4*>(ob + (size_t(yy) * a.img_w + iw * 16) * 2);
+          o16[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+          o16[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
         } else {
           uint32_t wd[4];
 #pragma unroll

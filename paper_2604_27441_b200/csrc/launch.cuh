@@ -83,6 +83,7 @@ struct EmbedTcArgs {
   __nv_bfloat16* qh; __nv_bfloat16* kh; __nv_bfloat16* vth;
   int b, h, w, nh, nw, ns, ns_pad;
   int x3;                         // precise: split operands (TcW emb3/qkv0_3), fp32 x
+  int u16;                        // frames are u16 depth planes (TcW emb16 / emb16_3)
 };
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 
@@ -137,6 +138,7 @@ struct LastTcArgs {
   const int32_t* out_slot;      //   frames + out_slot[b * slot_stride] * frame_bytes
   int slot_stride;
   size_t frame_bytes;
+  int u16;                      // u16 depth planes: out * 65535 quantisation, 2-byte pixels
   int max_hsplit;                // CTAs that may share a tile (1, 2 or 4)
 };
 bool last_tc_supported(const Dims& D, int b);

@@ -73,6 +73,25 @@ class RecoveryEngine:
             out = torch.empty((b, h, w, c), dtype=torch.uint8, device=frames.device)
         return nat.recover_u8(frames, frame_index, mask_bits, out, b, h, w, self.precision)
 
+    def recover_device16(self, frames: torch.Tensor, frame_index: torch.Tensor,
+                         mask_bits: torch.Tensor, out: torch.Tensor | None = None,
+                         in_place: bool = False, native=None) -> torch.Tensor | None:
+        """``recover_device`` for 16-bit depth planes (``nvrec_recover_u16``):
+        frames uint16 (n_slots, h, w) of a channels == 1 model, normalised as
+        u16 / 65535 and quantised as ``clip(out * 65535 + 0.5, 0, 65535)``."""
+        nat = native if native is not None else self.model.native(frames.device)
+        if self.channels != 1:
+            raise ValueError("16-bit planes need a depth (channels == 1) model")
+        if frames.dtype != torch.uint16 or frames.dim() != 3:
+            raise ValueError("frames must be uint16 (n_slots, h, w)")
+        _, h, w = frames.shape
+        b = frame_index.shape[0]
+        if in_place:
+            return nat.recover_u16(frames, frame_index, mask_bits, None, b, h, w, self.precision)
+        if out is None:
+            out = torch.empty((b, h, w), dtype=torch.uint16, device=frames.device)
+        return nat.recover_u16(frames, frame_index, mask_bits, out, b, h, w, self.precision)
+
     def recover(self, plane: np.ndarray, grid: np.ndarray, refs: list) -> np.ndarray:
         """Host-buffer call with ``_recover``'s signature and echo rules."""
         plane = np.asarray(plane)
@@ -269,24 +288,28 @@ class RecoveryPipeline:
         return self.lm[handle].status[:self.n, 0].cpu().numpy()
 
 
-def recover_depth16(model, plane: np.ndarray, grid: np.ndarray, refs: list) -> np.ndarray:
+def recover_depth16(model, plane: np.ndarray, grid: np.ndarray, refs: list,
+                    precision: str | None = None) -> np.ndarray:
     """16-bit depth extension of ``_recover`` (SPEC.md:74 calls 16-bit depth
     an extension point; the reference codec and wire format are u8-only).
 
-    Planes are u16 (h, w); the float module API is fed ``u16 / 65535`` (the
-    16-bit analogue of server.py:189), the output is quantised with
-    ``clip(out * 65535 + 0.5, 0, 65535)`` and merged through the block mask.
-    Use a ``precision="precise"`` model: it keeps the error below 1/65535 of
+    Planes are u16 (h, w), normalised as ``u16 / 65535`` (the 16-bit analogue
+    of server.py:189), the output quantised with ``clip(out * 65535 + 0.5, 0,
+    65535)`` and merged through the block mask -- all inside one
+    ``nvrec_recover_u16`` call (the u16 planes go to the device as they are;
+    the embedding reads each pixel as its two bytes).  Use the precise path
+    (the model's precision by default): it keeps the error below 1/65535 of
     full scale (the north_star's <= 1 mm at 1 mm per depth unit)."""
+    plane = np.asarray(plane)
     if not refs or not np.asarray(grid).any():
         return np.ascontiguousarray(plane)
     cfg = model.config
     dev = _native.require_cuda()
     refs = list(refs)[-cfg.k:]
-    host = np.stack(refs + [plane]).astype(np.uint16)
-    stack = torch.from_numpy(host.astype(np.int32)).to(dev).float().div_(65535.0)[None, :, None]
-    pix = np.repeat(np.repeat(np.asarray(grid, bool), MASK_BLOCK, 0), MASK_BLOCK, 1)
-    mask = torch.from_numpy(pix).to(dev)[None]
-    out = model(stack, mask)[0, 0]
-    q = torch.clamp(out * 65535.0 + 0.5, 0, 65535).to(torch.int32).cpu().numpy().astype(np.uint16)
-    return np.where(pix, q, plane)
+    host = np.stack([np.asarray(r, dtype=np.uint16) for r in refs] + [plane.astype(np.uint16)])
+    slots = stack_slots(len(refs), cfg.k, cfg.stack_len)
+    frames = torch.from_numpy(host).to(dev, non_blocking=True)
+    index = torch.tensor([slots], dtype=torch.int32).to(dev, non_blocking=True)
+    bits = torch.from_numpy(pack_grid(grid)[None]).to(dev, non_blocking=True)
+    eng = RecoveryEngine(model, precision or getattr(model, "precision", "precise"))
+    return eng.recover_device16(frames, index, bits)[0].cpu().numpy()

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_native.EXPORTS) == set(_declared())
-    assert lib.nvrec_abi_version() == _native.ABI_VERSION == 4
+    assert lib.nvrec_abi_version() == _native.ABI_VERSION == 5
 
 
 def test_sm100a_code_only():
