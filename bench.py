@@ -185,15 +185,25 @@ def stream_planes(c: int, h: int, w: int, sid: int, F: int = 6) -> np.ndarray:
     return np.stack([tex[i % 8: i % 8 + h, 0:w] for i in range(F)])
 
 
+def stream_planes16(h: int, w: int, sid: int, F: int = 6) -> np.ndarray:
+    """(F, h, w) u16 depth: 8x8-block depth steps (300..9000 units) drifting
+    one pixel per frame, slowly receding."""
+    rng = np.random.default_rng(16000 + 7919 * sid)
+    base = rng.integers(300, 9000, (h // 8 + 2, w // 8 + 2)).astype(np.uint16)
+    tex = np.kron(base, np.ones((8, 8), np.uint16))
+    return np.stack([tex[i % 8: i % 8 + h, 0:w] + np.uint16(3 * i) for i in range(F)])
+
+
 class Workload:
     """One BASELINE config: resolution, streams, and how a stream's loss mask
     arises -- ``("ge",)`` Gilbert-Elliott body-shard loss, ``("bern", p)``
     Bernoulli shard loss (both through the receiver/codec mask), or
     ``("block", r)`` a synthetic block mask (nvrec data.synthetic_mask)."""
 
-    def __init__(self, name, h, w, stream_ids, loss=("ge",)):
+    def __init__(self, name, h, w, stream_ids, loss=("ge",), depth16=False):
         self.name, self.h, self.w, self.loss = name, h, w, loss
         self.ids = list(stream_ids)
+        self.depth16 = depth16          # depth as u16 planes (nvrec_recover_u16)
 
     def planes(self, c, sid):
         return stream_planes(c, self.h, self.w, sid)
@@ -229,7 +239,8 @@ class Workload:
             kind = "Bernoulli %.0f%% body-shard loss" % (100 * self.loss[1])
         else:
             kind = "%.0f%% synthetic block mask (data.synthetic_mask)" % (100 * self.loss[1])
-        return "%dx%d RGB-D, %d streams, %s" % (self.w, self.h, len(self.ids), kind)
+        mod = "RGB + 16-bit depth" if self.depth16 else "RGB-D"
+        return "%dx%d %s, %d streams, %s" % (self.w, self.h, mod, len(self.ids), kind)
 
 
 class ModalityWork:
@@ -252,13 +263,18 @@ class ModalityWork:
         self.engine = engine
         self.engine.model.native(device)
         F = cfg.stack_len
-        self.host_frames = torch.empty((S * F, h, w, c), dtype=torch.uint8).pin_memory()
-        hf = self.host_frames.numpy().reshape(S, F, h, w, c)
+        # 16-bit depth: u16 (h, w) planes through nvrec_recover_u16
+        self.u16 = bool(wl.depth16 and c == 1)
+        shape = (h, w) if self.u16 else (h, w, c)
+        dt = torch.uint16 if self.u16 else torch.uint8
+        self.host_frames = torch.empty((S * F,) + shape, dtype=dt).pin_memory()
+        hf = self.host_frames.numpy().reshape((S, F) + shape)
         for s, sid in enumerate(wl.ids):
-            hf[s] = wl.planes(c, sid)
+            hf[s] = stream_planes16(h, w, sid) if self.u16 else wl.planes(c, sid)
         self.frames = self.host_frames.to(device)
-        self.ring_view = self.frames.view(S, F, h, w, c)
-        self.host_planes = self.host_frames.view(S, F, h, w, c)[:, -1].contiguous().pin_memory()
+        self.ring_view = self.frames.view((S, F) + shape)
+        self.host_planes = self.host_frames.view((S, F) + shape)[:, -1].contiguous().pin_memory()
+        self.recover = engine.recover_device16 if self.u16 else engine.recover_device
         self.index = torch.tensor([[s * F + i for i in stack_slots(5, 5, F)]
                                    for s in range(S)], dtype=torch.int32, device=device)
         nblk = (h // 16) * (w // 16)
@@ -280,8 +296,8 @@ class ModalityWork:
             self.host_wire = torch.from_numpy(bits).pin_memory()
             self.wire = self.host_wire.to(device)
         self.masked_patches = [int(g.sum()) for g in grids]
-        self.out = torch.empty((S, h, w, c), dtype=torch.uint8, device=device)
-        self.host_out = torch.empty((S, h, w, c), dtype=torch.uint8).pin_memory()
+        self.out = torch.empty((S,) + shape, dtype=dt, device=device)
+        self.host_out = torch.empty((S,) + shape, dtype=dt).pin_memory()
         self.pipe = None
         if pipeline and self.jobs is not None:
             from paper_2604_27441_b200.recovery import RecoveryPipeline
@@ -304,7 +320,7 @@ class ModalityWork:
         the corrupted plane's slot; the model never reads those pixels, so
         repeating the step recomputes the same plane)."""
         self._mask(stream)
-        self.engine.recover_device(self.frames, self.index, self.wire, in_place=True)
+        self.recover(self.frames, self.index, self.wire, in_place=True)
 
     def e2e_step(self, stream):
         """Unpipelined end to end: H2D of each stream's corrupted plane and
@@ -315,7 +331,7 @@ class ModalityWork:
         else:
             self.wire.copy_(self.host_wire, non_blocking=True)
         self.ring_view[:, -1].copy_(self.host_planes, non_blocking=True)
-        self.engine.recover_device(self.frames, self.index, self.wire, self.out)
+        self.recover(self.frames, self.index, self.wire, self.out)
         self.ring_view[:, -2].copy_(self.out, non_blocking=True)   # ring push
         self.host_out.copy_(self.out, non_blocking=True)
 
@@ -329,13 +345,13 @@ class ModalityWork:
 
     def h2d_bytes(self):
         m = self.lm.h2d_bytes if self.lm is not None else self.host_wire.numel()
-        return int(m + self.host_planes.numel())
+        return int(m + self.host_planes.numel() * self.host_planes.element_size())
 
     def h2d_bytes_protocol(self):
         return int(self.lm.h2d_bytes + self.host_frames.numel())
 
     def d2h_bytes(self):
-        return int(self.host_out.numel())
+        return int(self.host_out.numel() * self.host_out.element_size())
 
 
 class ReceiverWork:
@@ -747,6 +763,8 @@ def main():
         cfgs = [
             ("configs[0] 320x240 10% block", Workload("c0", 240, 320, mine, ("block", 0.10))),
             ("configs[1] 640x480 Bernoulli 5%", Workload("c1", 480, 640, mine, ("bern", 0.05))),
+            ("configs[1] 640x480 RGB + 16-bit depth, Bernoulli 5%",
+             Workload("c1d16", 480, 640, mine, ("bern", 0.05), depth16=True)),
             ("configs[2] 720p 10% block", Workload("c2b10", H, W, mine, ("block", 0.10))),
             ("configs[2] 720p 20% block", Workload("c2b20", H, W, mine, ("block", 0.20))),
             ("configs[3] 1920x1088 20% block", Workload("c3", 1088, 1920, mine, ("block", 0.20))),
