@@ -4,6 +4,13 @@
 //   mode 2: tcgen05.mma kind::f16 M128 N32 K16 with A from TMEM (PV shape),
 //           one thread issuing back to back (A read: 128 lanes x 8 cols x 4 B)
 //   mode 3: same MMA shape with A from shared memory (SS)
+//   mode 4: SS MMAs issued by one thread in each of `warps` warps (own
+//           accumulators): is the ~44 clk/MMA floor at small N per issuer?
+//   mode 6: the dense precise attention's MMA stream per S tile, no softmax:
+//           S = 6 x (M128 N128 K16, SWIZZLE_128B Q/K) into buffer n % 3, then
+//           PV = 8 x (N64 A=TMEM + N32 A=TMEM) into O; clk per S tile
+//   mode 5: SS MMAs by warp 0 while warps 1..warps-1 stream tcgen05.ld over
+//           TMEM columns 0-255 (the softmax's S reads): TMEM contention
 // One CTA per SM, all 148 SMs; clock64 deltas per CTA.  Prints bytes/clk/SM.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_2604_27441_b200/csrc
 //        ubench_tmem.cu -o ubench_tmem -lcuda
@@ -23,12 +30,14 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
   __shared__ uint32_t tbase;
   __shared__ __align__(1024) uint8_t a_smem[128 * 16 * 2];
   __shared__ __align__(1024) uint8_t b_smem[256 * 16 * 2];
-  __shared__ uint64_t bar;
+  __shared__ __align__(1024) uint8_t q_smem[kMode == 6 ? 32768 + 16384 - 8192 : 16];
+  __shared__ uint64_t bar, bars[16];
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < int(sizeof(a_smem)); i += blockDim.x) a_smem[i] = 0;
   for (int i = threadIdx.x; i < int(sizeof(b_smem)); i += blockDim.x) b_smem[i] = 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    for (int i = 0; i < 16; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(&tbase);
@@ -58,6 +67,68 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
         } else {
           tmem_wait_st();
         }
+      }
+    }
+  } else if (kMode == 4) {
+    if ((threadIdx.x & 31) == 0 && warp < warps) {
+      const uint32_t idesc = idesc_bf16(128, kN);
+      const uint64_t bd = sdesc(smem_u32(b_smem), 128, kSwizzleNone, 256);
+      const uint64_t ad = sdesc(smem_u32(a_smem), 128, kSwizzleNone, 2048);
+      const uint32_t d = t + warp * kN;
+      for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mma_ss(d, ad, bd, idesc, 1);
+      }
+      mma_commit(&bars[warp]);
+      mbar_wait(&bars[warp], 0);
+    }
+  } else if (kMode == 6) {
+    if (threadIdx.x == 0) {
+      const uint32_t qb = smem_u32(q_smem), kb = qb + 8192, vb = qb + 24576;   // overlapping: timing only
+      constexpr uint32_t idS = idesc_bf16(128, 128), idP64 = idesc_bf16(128, 64),
+                         idP32 = idesc_bf16(128, 32);
+      constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
+      for (int n = 0; n < kIters; ++n) {
+        const uint32_t sc = t + (n % 3) * 128;
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+          mma_ss(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
+                 sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
+        if (n >= 2) {
+          const uint32_t bc = t + ((n - 2) % 3) * 128, oc = t + 384;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
+            const uint32_t vh = vb + (kk >> 2) * 8192 + (kk & 3) * 32;
+            mma_ts(oc, ah, sdesc(vh, 1024, kSwizzle128B), idP64, kk);
+            mma_ts(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), idP32, 1);
+          }
+        }
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+    }
+  } else if (kMode == 5) {
+    if (threadIdx.x == 0) {
+      const uint32_t idesc = idesc_bf16(128, kN);
+      const uint64_t bd = sdesc(smem_u32(b_smem), 128, kSwizzleNone, 256);
+      const uint64_t ad = sdesc(smem_u32(a_smem), 128, kSwizzleNone, 2048);
+      for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mma_ss(t + 256 + (c & 1) * 128, ad, bd, idesc, 1);
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
+      sink[1] = 1;
+    } else if (warp >= 4 && warp < 4 + warps) {
+      const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
+      uint32_t r[32];
+      volatile uint32_t* flag = sink + 1;
+      for (int it = 0; it < 4 * kIters && *flag == 0; ++it) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(t + lane_off + ((64 * c + 32 * (warp >> 2)) & 255), r);
+        tmem_wait_ld();
+        acc ^= r[it & 31];
       }
     }
   } else {
@@ -92,17 +163,20 @@ void run(const char* name, int warps, double bytes_per_cta) {
   unsigned long long* cyc;
   uint32_t* sink;
   cudaMalloc(&cyc, 148 * 8);
-  cudaMalloc(&sink, 4);
+  cudaMalloc(&sink, 8);
+  cudaMemset(sink, 0, 8);
   tmem_bench<kMode, kN, kAcc><<<148, 512>>>(cyc, sink, warps);
   cudaDeviceSynchronize();
+  cudaMemset(sink, 0, 8);
   tmem_bench<kMode, kN, kAcc><<<148, 512>>>(cyc, sink, warps);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
   double mean = 0;
   for (int i = 0; i < 148; ++i) mean += double(h[i]) / 148;
-  printf("%-34s N=%3d acc=%d warps=%2d  %8.1f bytes/clk/SM  (%.0f clk, %.1f clk/MMA, %s)\n", name,
-         kN, kAcc, warps, bytes_per_cta / mean, mean, mean / (kIters * 8.0), cudaGetErrorString(e));
+  printf("%-34s N=%3d acc=%d warps=%2d  %8.1f bytes/clk/SM  (%.0f clk, %.1f clk/%s, %s)\n", name,
+         kN, kAcc, warps, bytes_per_cta / mean, mean, mean / (kIters * (kMode == 6 ? 1.0 : 8.0)),
+         kMode == 6 ? "S tile" : "MMA", cudaGetErrorString(e));
   cudaFree(cyc);
   cudaFree(sink);
 }
@@ -129,6 +203,13 @@ int main() {
   run<3, 128, 2>("mma A=SMEM", 1, ab);
   run<3, 256, 1>("mma A=SMEM", 1, ab);
   run<3, 256, 2>("mma A=SMEM", 1, ab);
+  for (int w : {1, 2, 4})
+    run<4, 32, 1>("mma SS N32, one issuer per warp", w, ab * w);
+  for (int w : {1, 2, 4})
+    run<4, 64, 1>("mma SS N64, one issuer per warp", w, ab * w);
+  for (int w : {0, 4, 8})
+    run<5, 128, 1>("mma SS N128 + LDTM warps", w, ab);
+  run<6, 128, 1>("x3w MMA stream (S 6xN128 + PV 8x(N64+N32))", 1, ab);
   run<2, 64, 1>("mma A=TMEM", 1, ab);
   run<2, 128, 1>("mma A=TMEM", 1, ab);
   return 0;
