@@ -9,6 +9,8 @@
 //   mode 6: the dense precise attention's MMA stream per S tile, no softmax:
 //           S = 6 x (M128 N128 K16, SWIZZLE_128B Q/K) into buffer n % 3, then
 //           PV = 8 x (N64 A=TMEM + N32 A=TMEM) into O; clk per S tile
+//   mode 7: mode 6 while warps 4.. stream the softmax's TMEM traffic (two
+//           tcgen05.ld x32 + four tcgen05.st x16 per 64 columns) over the S buffers
 //   mode 5: SS MMAs by warp 0 while warps 1..warps-1 stream tcgen05.ld over
 //           TMEM columns 0-255 (the softmax's S reads): TMEM contention
 // One CTA per SM, all 148 SMs; clock64 deltas per CTA.  Prints bytes/clk/SM.
@@ -30,7 +32,7 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
   __shared__ uint32_t tbase;
   __shared__ __align__(1024) uint8_t a_smem[128 * 16 * 2];
   __shared__ __align__(1024) uint8_t b_smem[256 * 16 * 2];
-  __shared__ __align__(1024) uint8_t q_smem[kMode == 6 ? 32768 + 16384 - 8192 : 16];
+  __shared__ __align__(1024) uint8_t q_smem[kMode >= 6 ? 32768 + 16384 - 8192 : 16];
   __shared__ uint64_t bar, bars[16];
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < int(sizeof(a_smem)); i += blockDim.x) a_smem[i] = 0;
@@ -82,7 +84,26 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
       mma_commit(&bars[warp]);
       mbar_wait(&bars[warp], 0);
     }
-  } else if (kMode == 6) {
+  } else if (kMode == 6 || kMode == 7) {
+    if (kMode == 7 && warp >= 4 && warp < 4 + warps) {
+      const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
+      uint32_t r[64];
+      volatile uint32_t* flag = sink + 1;
+      for (int it = 0; it < 64 * kIters && *flag == 0; ++it) {
+        const uint32_t c0 = ((it + warp) % 6) * 64;
+        tmem_ld32(t + lane_off + c0, r);
+        tmem_ld32(t + lane_off + c0 + 32, r + 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] ^= r[i + 32];
+        tmem_st16(t + lane_off + c0, r);
+        tmem_st16(t + lane_off + c0 + 16, r + 16);
+        tmem_st16(t + lane_off + c0 + 32, r);
+        tmem_st16(t + lane_off + c0 + 48, r + 16);
+        tmem_wait_st();
+        acc ^= r[it & 31];
+      }
+    }
     if (threadIdx.x == 0) {
       const uint32_t qb = smem_u32(q_smem), kb = qb + 8192, vb = qb + 24576;   // overlapping: timing only
       constexpr uint32_t idS = idesc_bf16(128, 128), idP64 = idesc_bf16(128, 64),
@@ -107,6 +128,7 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
       }
       mma_commit(&bar);
       mbar_wait(&bar, 0);
+      sink[1] = 1;
     }
   } else if (kMode == 5) {
     if (threadIdx.x == 0) {
@@ -175,8 +197,8 @@ void run(const char* name, int warps, double bytes_per_cta) {
   double mean = 0;
   for (int i = 0; i < 148; ++i) mean += double(h[i]) / 148;
   printf("%-34s N=%3d acc=%d warps=%2d  %8.1f bytes/clk/SM  (%.0f clk, %.1f clk/%s, %s)\n", name,
-         kN, kAcc, warps, bytes_per_cta / mean, mean, mean / (kIters * (kMode == 6 ? 1.0 : 8.0)),
-         kMode == 6 ? "S tile" : "MMA", cudaGetErrorString(e));
+         kN, kAcc, warps, bytes_per_cta / mean, mean, mean / (kIters * (kMode >= 6 ? 1.0 : 8.0)),
+         kMode >= 6 ? "S tile" : "MMA", cudaGetErrorString(e));
   cudaFree(cyc);
   cudaFree(sink);
 }
@@ -210,6 +232,8 @@ int main() {
   for (int w : {0, 4, 8})
     run<5, 128, 1>("mma SS N128 + LDTM warps", w, ab);
   run<6, 128, 1>("x3w MMA stream (S 6xN128 + PV 8x(N64+N32))", 1, ab);
+  for (int w : {4, 8})
+    run<7, 128, 1>("x3w MMA stream + softmax TMEM ld/st", w, ab);
   run<2, 64, 1>("mma A=TMEM", 1, ab);
   run<2, 128, 1>("mma A=TMEM", 1, ab);
   return 0;
