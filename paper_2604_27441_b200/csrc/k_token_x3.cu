@@ -51,6 +51,17 @@ struct __align__(128) X3Smem {
   uint32_t tmem_base;
 };
 
+#ifdef NVREC_TRACE
+// phase timestamps of CTA 0, slot 0, its first two tiles (tools/trace_token.py)
+__device__ unsigned long long g_tx_trace[3][2][16];
+#define TX(i) \
+  do { \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ntile < 2) g_tx_trace[PH][ntile][i] = clock64(); \
+  } while (0)
+#else
+#define TX(i) do {} while (0)
+#endif
+
 template <int PH>
 __global__ void __launch_bounds__(kThreads, 1)
 token_x3_kernel(TokenX3Args a) {
@@ -147,7 +158,9 @@ token_x3_kernel(TokenX3Args a) {
   };
   const float scale = rsqrtf(32.f);
 
-  for (int tile = blockIdx.x * kSlots + slot; tile < n_tiles; tile += gridDim.x * kSlots) {
+  int ntile = 0;
+  for (int tile = blockIdx.x * kSlots + slot; tile < n_tiles; tile += gridDim.x * kSlots, ++ntile) {
+    TX(0);
     const int b = tile / tiles_per_b;
     const int s = (tile - b * tiles_per_b) * P + wq * ppw + jl;
     const bool valid = row_live && s < a.ns;
@@ -171,13 +184,17 @@ token_x3_kernel(TokenX3Args a) {
           y[4 * q] = u.x; y[4 * q + 1] = u.y; y[4 * q + 2] = u.z; y[4 * q + 3] = u.w;
         }
       }
+      TX(1);
       put_row_x3(A, m, y);
       gemm_a(0, kX3ProjS, 64);
+      TX(2);
       add64(x, 0, a.sc[0], P_ + kPBProjS);
       // ---- qkv_t(LN_t(x)); temporal attention by warp shuffles ----------------
       layernorm64(x, y, P_ + kPLnTw, P_ + kPLnTb);
       put_row_x3(A, m, y);
+      TX(3);
       gemm_a(0, kX3QkvT, 192);
+      TX(4);
       const float sq = a.sc[1];
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
@@ -228,7 +245,9 @@ token_x3_kernel(TokenX3Args a) {
         put_row_x3(A, m, q, 4 * hh, 4);                // head hh -> A columns [32hh, 32hh+32)
       }
       // ---- x += proj_t(o) ------------------------------------------------------
+      TX(5);
       gemm_a(0, kX3ProjT, 64);
+      TX(6);
       add64(x, 0, a.sc[2], P_ + kPBProjT);
       if (valid) {
         float4* xo = reinterpret_cast<float4*>(a.x + xrow);
@@ -237,8 +256,10 @@ token_x3_kernel(TokenX3Args a) {
       }
     } else if constexpr (PH == 1) {
       // ---- x += fc2(GELU(fc1(LN_m(x)))) in two halves of 128 hidden units ------
+      TX(1);
       layernorm64(x, y, P_ + kPLnMw, P_ + kPLnMb);
       put_row_x3(A, m, y);
+      TX(2);
       const float s1 = a.sc[3], s2 = a.sc[4];
       // fc2 K step kk (16 hidden units of half H) from the TMEM column groups
       auto issue_fc2 = [&](int H) {
@@ -259,6 +280,7 @@ token_x3_kernel(TokenX3Args a) {
       for (int H = 0; H < 2; ++H) {
         if (H == 0) run([&] { issue_a(0, kX3Fc1, 128, 256, 0); });
         else run([&] { issue_fc2(0); issue_a(0, kX3Fc1, 128, 256, 128); });
+        TX(3 + 2 * H);
 #pragma unroll 1
         for (int g = 0; g < 2; ++g) {
           uint32_t r[64], lo[32];
@@ -268,16 +290,18 @@ token_x3_kernel(TokenX3Args a) {
           const float* bias = P_ + kPBFc1 + 128 * H + 64 * g;
 #pragma unroll
           for (int e = 0; e < 64; e += 2)
-            split_h2(gelu_erf(fmaf(__uint_as_float(r[e]), s1, bias[e])),
-                     gelu_erf(fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])), r[e / 2], lo[e / 2]);
+            split_h2(gelu_as(fmaf(__uint_as_float(r[e]), s1, bias[e])),
+                     gelu_as(fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])), r[e / 2], lo[e / 2]);
           tmem_st16(tbase + lane_off + 64 * g, r);
           tmem_st16(tbase + lane_off + 64 * g + 16, r + 16);
           tmem_st16(tbase + lane_off + 64 * g + 32, lo);
           tmem_st16(tbase + lane_off + 64 * g + 48, lo + 16);
         }
         tmem_wait_st();
+        TX(4 + 2 * H);
       }
       run([&] { issue_fc2(1); });
+      TX(7);
       add64(x, 128, s2, P_ + kPBFc2);
       if (valid) {
         float4* xo = reinterpret_cast<float4*>(a.x + xrow);
@@ -286,12 +310,17 @@ token_x3_kernel(TokenX3Args a) {
       }
     } else {
       // ---- next block's LN_s + qkv_s -> split bf16 attention operands ----------
+      TX(1);
       layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
       put_row_x3(A, m, y);
+      TX(2);
       gemm_a(0, kX3QkvS, 192);
+      TX(3);
       int qrow = s;
       if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
       const float sq = a.sc[5];
+      __nv_bfloat16* vt = reinterpret_cast<__nv_bfloat16*>(A);
+      const int jpos = wq * ppw + jl;                 // position inside the tile
 #pragma unroll 1
       for (int c6 = 0; c6 < 6; ++c6) {
         uint32_t r[32];
@@ -316,17 +345,42 @@ token_x3_kernel(TokenX3Args a) {
             d4[4 + e / 8] = make_uint4(l[0], l[1], l[2], l[3]);
           }
         } else {
-          __nv_bfloat16* dst = a.vth + seq * 64 * a.ns_pad + s;
+          // V^T rows (hi e, lo 32 + e) staged in the slot's A buffer (the qkv_s
+          // MMA has consumed it) as [slice, head][64][position]
+          __nv_bfloat16* st = vt + ((it * 2 + head) * 64) * P + jpos;
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const __nv_bfloat16 h = __float2bfloat16_rn(v[e]);
-            dst[size_t(e) * a.ns_pad] = h;
-            dst[size_t(32 + e) * a.ns_pad] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
+            st[e * P] = h;
+            st[(32 + e) * P] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
           }
         }
       }
+      // coalesced V^T stores: 8 consecutive positions (16 bytes) per store
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+      {
+        const int s0 = (tile - b * tiles_per_b) * P;
+        const int nvalid = min(P, a.ns - s0);
+        const int cpr = (P + 7) / 8;                     // chunks per staged row
+        const int rows = nt * 2 * 64;
+        for (int idx = m; idx < rows * cpr; idx += 128) {
+          const int row = idx / cpr, ch = idx - row * cpr;
+          const int sl = row >> 6, e = row & 63;
+          const size_t seq = size_t(b * nt + (sl >> 1)) * 2 + (sl & 1);
+          __nv_bfloat16* dst = a.vth + (seq * 64 + e) * a.ns_pad + s0 + 8 * ch;
+          const __nv_bfloat16* src = vt + row * P + 8 * ch;
+          if ((P & 7) == 0 && 8 * ch + 8 <= nvalid) {
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+          } else {
+            for (int k = 0; k < 8 && 8 * ch + k < nvalid; ++k) dst[k] = src[k];
+          }
+        }
+      }
+      // the staging buffer is the next tile's A operand
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
     }
     // every thread's TMEM reads precede the next tile's first MMA (run()'s barrier)
+    TX(15);
   }
   tc_fence_before();
   __syncthreads();
@@ -347,6 +401,14 @@ cudaError_t launch_phase(const TokenX3Args& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef NVREC_TRACE
+int token_x3_trace(unsigned long long* host, int n) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int m = n < 96 ? n : 96;
+  return cudaMemcpyFromSymbol(host, g_tx_trace, m * 8) == cudaSuccess ? m : -1;
+}
+#endif
 
 cudaError_t launch_token_x3(const TokenX3Args& a, cudaStream_t s) {
   cudaError_t e;
