@@ -11,6 +11,8 @@
 //           PV = 8 x (N64 A=TMEM + N32 A=TMEM) into O; clk per S tile
 //   mode 7: mode 6 while warps 4.. stream the softmax's TMEM traffic (two
 //           tcgen05.ld x32 + four tcgen05.st x16 per 64 columns) over the S buffers
+//   mode 8: mode 6 with the kernel's per-S-tile tcgen05.commit pattern (after
+//           the S MMAs, after the PV MMAs, and a K/V-release commit)
 //   mode 5: SS MMAs by warp 0 while warps 1..warps-1 stream tcgen05.ld over
 //           TMEM columns 0-255 (the softmax's S reads): TMEM contention
 // One CTA per SM, all 148 SMs; clock64 deltas per CTA.  Prints bytes/clk/SM.
@@ -83,6 +85,39 @@ __global__ void __launch_bounds__(512, 1) tmem_bench(unsigned long long* cyc, ui
       }
       mma_commit(&bars[warp]);
       mbar_wait(&bars[warp], 0);
+    }
+  } else if (kMode == 8) {
+    if (threadIdx.x == 0) {
+      const uint32_t qb = smem_u32(q_smem), kb = qb + 8192, vb = qb + 24576;
+      constexpr uint32_t idS = idesc_bf16(128, 128), idP64 = idesc_bf16(128, 64),
+                         idP32 = idesc_bf16(128, 32);
+      constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
+      for (int n = 0; n < kIters; ++n) {
+        const uint32_t sc = t + (n % 3) * 128;
+        if (warps & 8) tc_fence_after();
+        if (warps & 16) mbar_wait_fast(&bars[15], 1);     // an already-completed phase
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+          mma_ss(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
+                 sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
+        if (warps & 1) mma_commit(&bars[n % 3]);
+        if (warps & 8) tc_fence_after();
+        if (warps & 16) mbar_wait_fast(&bars[15], 1);
+        if (n >= 2) {
+          const uint32_t bc = t + ((n - 2) % 3) * 128, oc = t + 384;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
+            const uint32_t vh = vb + (kk >> 2) * 8192 + (kk & 3) * 32;
+            mma_ts(oc, ah, sdesc(vh, 1024, kSwizzle128B), idP64, kk);
+            mma_ts(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), idP32, 1);
+          }
+          if (warps & 2) mma_commit(&bars[3 + (n & 1)]);
+          if (warps & 4) mma_commit(&bars[5 + (n & 3)]);
+        }
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, 0);
     }
   } else if (kMode == 6 || kMode == 7) {
     if (kMode == 7 && warp >= 4 && warp < 4 + warps) {
@@ -234,6 +269,8 @@ int main() {
   run<6, 128, 1>("x3w MMA stream (S 6xN128 + PV 8x(N64+N32))", 1, ab);
   for (int w : {4, 8})
     run<7, 128, 1>("x3w MMA stream + softmax TMEM ld/st", w, ab);
+  for (int w : {0, 1, 3, 7, 15, 23, 31})   // bit 0: commit after S, 1: after PV, 2: K/V release, 3: fence::after_thread_sync x2, 4: mbarrier try_wait x2
+    run<8, 128, 1>("x3w MMA stream + commits (mask)", w, ab);
   run<2, 64, 1>("mma A=TMEM", 1, ab);
   run<2, 128, 1>("mma A=TMEM", 1, ab);
   return 0;
