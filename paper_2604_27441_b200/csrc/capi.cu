@@ -638,7 +638,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
             for (int px = 0; px < p; ++px) emx = std::fmax(emx, std::fabs(ew_at(o, ci, tt, py, px)));
     const int se = exponent_for(emx);
     m->W.tc.sc_emb = std::ldexp(1.f, -se);
-    const int kpy3 = c == 3 ? 2 : 4, kst3 = 16 * kpy3 * c;   // embed_tc's K stage (EmbSmem::kPy)
+    const int kpy3 = c == 3 ? 1 : 2, kst3 = 16 * kpy3 * c;   // embed_tc's X3 K stage (EmbSmem::kPy)
     size_t emb3_off = 0;
     for (int st = 0; st < T * 16 / kpy3; ++st) {
       const int tt = st / (16 / kpy3), py0 = kpy3 * (st % (16 / kpy3));
@@ -671,8 +671,8 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     if (c == 1) {
       const int s16 = exponent_for(256.f * emx);
       m->W.tc.sc_emb16 = std::ldexp(1.f, -s16);
-      for (int st = 0; st < T * 8; ++st) {
-        const size_t o = pack2(d, 64, at16(st / 8, 2 * (st % 8)), s16);
+      for (int st = 0; st < T * 16; ++st) {             // one patch row per X3 stage
+        const size_t o = pack2(d, 32, at16(st / 16, st % 16), s16);
         if (st == 0) emb16_3_off = o;
       }
     }

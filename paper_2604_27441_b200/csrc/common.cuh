@@ -112,7 +112,7 @@ struct TcW {
   // W * 2^s (hi = fp16(W 2^s), lo = fp16(W 2^s - hi); s per matrix puts
   // max|W| 2^s near 2^14 so lo stays a normal number); sc = 2^-s undoes it in
   // the epilogue.  Same element order as the fast packs.
-  const __half* emb3;           // [T*16/kPy stages][hi 64 x 16 kPy c | lo ...], kPy = 2 (RGB) / 4
+  const __half* emb3;           // [T*16/kPy stages][hi 64 x 16 kPy c | lo ...], kPy = 1 (RGB) / 2
   const __half* qkv0_3;         // [hi 192x64 | lo 192x64] block-0 qkv_s
   const __half* blk3[8];        // per block: proj_s | qkv_t | proj_t | fc1 | fc2 | qkv_s, each [hi | lo]
   // head rows of the last tubelet frame in 4 chunks of 4 patch rows (64c

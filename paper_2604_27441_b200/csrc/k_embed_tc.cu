@@ -57,7 +57,9 @@ constexpr int kThreads = 192;
 template <int C, bool X3 = false>
 struct __align__(128) EmbSmem {
   static constexpr int kX = X3 ? 2 : 1;                      // hi (+ lo) operand copies
-  static constexpr int kPy = C == 1 ? 4 : 2;                 // patch rows per K stage
+  // patch rows per K stage; the split-operand (X3) variants use half-size
+  // stages so that two CTAs fit on an SM (<= ~113 KB of shared memory each)
+  static constexpr int kPy = X3 ? (C == 1 ? 2 : 1) : (C == 1 ? 4 : 2);
   static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame
   // A/W (MMA operand) ring: 2 stages for both modalities (a 3-stage depth
   // ring measured the same 79.6 us per 8 x 720p launch and trips
@@ -413,7 +415,7 @@ cudaError_t launch_c(const EmbedTcArgs& a, cudaStream_t s) {
                         cuuint64_t(a.n_slots)};
   cuuint64_t strides[4] = {cuuint64_t(16 * C), cuuint64_t(a.w) * C, cuuint64_t(16) * a.w * C,
                            cuuint64_t(a.h) * a.w * C};
-  cuuint32_t box[5] = {cuuint32_t(16 * C), kTw, EmbSmem<C>::kPy, kTh, 1};
+  cuuint32_t box[5] = {cuuint32_t(16 * C), kTw, EmbSmem<C, X3>::kPy, kTh, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(a.frames), dims, strides,
          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
