@@ -65,7 +65,10 @@ struct __align__(128) EmbSmem {
   // ring measured the same 79.6 us per 8 x 720p launch and trips
   // compute-sanitizer synccheck's mbarrier tracking)
   static constexpr int kNst = 2;
-  static constexpr int kNu8 = C == 1 ? 4 : 3;                // raw-pixel TMA ring
+  static constexpr uint32_t kU8_ = kTh * kPy * kTw * 16 * C;
+  // raw-pixel TMA ring: the X3 variants fill the region the LN output (A2,
+  // 32 KB) needs anyway -- 5-8 stages in flight against HBM latency
+  static constexpr int kNu8 = X3 ? int(32768 / kU8_) : (C == 1 ? 4 : 3);
   static constexpr uint32_t kU8 = kTh * kPy * kTw * 16 * C; // raw pixels per stage
   static constexpr uint32_t kA = kRows * 16 * kPy * C * 2;  // fp16 A per stage
   static constexpr uint32_t kW1 = 64 * 16 * kPy * C * 2;    // fp16 W per stage (one copy)
