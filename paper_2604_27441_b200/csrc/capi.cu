@@ -185,6 +185,14 @@ bool precise_simt() {
   return on;
 }
 
+bool f32_embed_simt() {   // NVREC_F32_EMBED_SIMT=1: the float API embeds on CUDA cores (A/B)
+  static const bool on = [] {
+    const char* e = getenv("NVREC_F32_EMBED_SIMT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool last_simt() {
   static const bool on = [] {
     const char* e = getenv("NVREC_LAST_SIMT");
@@ -590,6 +598,21 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
         const size_t o = pack(d, 64, at16(st / 8, 2 * (st % 8)));
         if (st == 0) emb16_off = o;
       }
+    // float module-API embedding (k_embed_tc.cu, F32): stages of 2 rows of one
+    // channel (tt, ch, rp), then the mask channel's 8 stages (last sub-frame)
+    auto atf = [&](int st) {
+      const int nimg = T * c * 8;
+      const int tt = st < nimg ? st / (c * 8) : T - 1;
+      const int ch = st < nimg ? (st / 8) % c : c;
+      const int rp = st < nimg ? st % 8 : st - nimg;
+      return [&, tt, ch, rp](int n, int k) { return ew_at(n, ch, tt, 2 * rp + k / 16, k % 16); };
+    };
+    const int nstf = T * c * 8 + 8;
+    size_t embf_off = 0;
+    for (int st = 0; st < nstf; ++st) {
+      const size_t o = pack(d, 32, atf(st));
+      if (st == 0) embf_off = o;
+    }
     CK(cudaMalloc(&m->blob_bf16, hb.size() * sizeof(__half)), "cudaMalloc(fp16)");
     CK(cudaMemcpy(m->blob_bf16, hb.data(), hb.size() * sizeof(__half),
                   cudaMemcpyHostToDevice), "cudaMemcpy(fp16)");
@@ -598,6 +621,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     m->W.tc.qkv0 = m->blob_bf16 + qoff;
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk[i] = m->blob_bf16 + blk_pack[i];
     m->W.tc.emb16 = emb16_off == SIZE_MAX ? nullptr : m->blob_bf16 + emb16_off;
+    m->W.tc.embf = m->blob_bf16 + embf_off;
 
     // ---- split-fp16 [hi | lo] packs for the precise path ----------------------
     // W * 2^s with max|W| 2^s in [2^13, 2^14): hi = fp16(W 2^s) and lo =
@@ -676,6 +700,20 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
         if (st == 0) emb16_3_off = o;
       }
     }
+    // float module-API embedding, split: one exponent over image + mask channels
+    size_t embf3_off = 0;
+    {
+      float fmx = emx;
+      for (int o = 0; o < d; ++o)
+        for (int py = 0; py < p; ++py)
+          for (int px = 0; px < p; ++px) fmx = std::fmax(fmx, std::fabs(ew_at(o, c, T - 1, py, px)));
+      const int sf = exponent_for(fmx);
+      m->W.tc.sc_embf = std::ldexp(1.f, -sf);
+      for (int st = 0; st < nstf; ++st) {
+        const size_t o = pack2(d, 32, atf(st), sf);
+        if (st == 0) embf3_off = o;
+      }
+    }
     // head (last tubelet frame rows, model.py:119-120) in 4 chunks of 4 patch
     // rows = 64c columns: the last-block kernel streams one chunk at a time
     const float* hw3 = t[tail + 2];
@@ -717,6 +755,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     for (int i = 0; i < D.layers; ++i) m->W.tc.blk3[i] = m->blob_x3 + blk3[i];
     m->W.tc.head3 = m->blob_x3 + head3_off;
     m->W.tc.emb16_3 = emb16_3_off == SIZE_MAX ? nullptr : m->blob_x3 + emb16_3_off;
+    m->W.tc.embf3 = m->blob_x3 + embf3_off;
     m->W.tc.last3 = m->blob_x3 + last3_off;
   }
   m->loaded = true;
@@ -825,8 +864,29 @@ int nvrec_forward_f32(const nvrec_model* m, const float* stack, int32_t b, int32
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   nvrec::Act A = make_act(m, ws, L, b, h, w);
   const int am = attn_mode(m->D, precision);
-  rc = embed_and_qkv0(m, A, false, stack, f, mask, nullptr, nullptr, h, w, false, precision, s);
-  if (rc) return rc;
+  if (am && nvrec::embed_tc_supported(m->D) && m->W.tc.embf && !precise_simt() &&
+      !f32_embed_simt()) {
+    // tcgen05 embedding of the float stack (+ block-0 LN/QKV), k_embed_tc.cu F32
+    nvrec::EmbedTcArgs ea{};
+    ea.f32 = 1;
+    ea.x3 = am == 2;
+    ea.D = m->D;
+    ea.tcw = &m->W.tc;
+    ea.emb_wmsum = m->W.emb_wmsum; ea.emb_b = m->W.emb_b; ea.time_pos = m->W.time_pos;
+    ea.ln_w = m->W.blk[0].ln_s_w; ea.ln_b = m->W.blk[0].ln_s_b; ea.qkv_b = m->W.blk[0].qkv_s_b;
+    ea.stack = stack; ea.f_in = f; ea.pmask = mask;
+    ea.x = A.x; ea.qh = A.qh; ea.kh = A.kh; ea.vth = A.vth;
+    ea.b = b; ea.h = h; ea.w = w; ea.nh = A.nh; ea.nw = A.nw; ea.ns = A.ns; ea.ns_pad = A.ns_pad;
+    cudaError_t e2;
+    {
+      ProfScope ps(NVREC_STAGE_EMBED, s);
+      e2 = nvrec::launch_embed_tc(ea, s);
+    }
+    if (e2 != cudaSuccess) return cuda_fail(e2, "embed_tc (f32) launch");
+  } else {
+    rc = embed_and_qkv0(m, A, false, stack, f, mask, nullptr, nullptr, h, w, false, precision, s);
+    if (rc) return rc;
+  }
   return run_blocks(m, A, L, am, false, h, w, out, nullptr, s);
 }
 

@@ -125,6 +125,12 @@ struct TcW {
   const __half* emb16;
   const __half* emb16_3;
   float sc_emb16;
+  // float module-API embedding (k_embed_tc.cu, F32): per stage 2 pixel rows
+  // (K = 32) of one channel of one sub-frame, T x c x 8 stages, then 8
+  // mask-channel stages (last sub-frame); fp16 (embf) and [hi | lo] x 2^s (embf3)
+  const __half* embf;
+  const __half* embf3;
+  float sc_embf;
   // the last block's matrices as k_last_tc.cu streams them: proj_s | qkv_t |
   // proj_t | fc1 rows 0-127 | fc1 rows 128-255 | fc2 K 0-127 | fc2 K 128-255,
   // each [hi | lo] (scales sc_blk[layers - 1])

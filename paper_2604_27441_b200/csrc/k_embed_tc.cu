@@ -54,24 +54,25 @@ constexpr int kThreads = 192;
 // is done.  A K stage is kPy patch rows of one tubelet frame: 2 for RGB
 // (K = 96), 4 for depth (K = 64) so a depth stage is not dominated by its
 // barrier round trip.
-template <int C, bool X3 = false>
+template <int C, bool X3 = false, bool F32 = false>
 struct __align__(128) EmbSmem {
   static constexpr int kX = X3 ? 2 : 1;                      // hi (+ lo) operand copies
   // patch rows per K stage; the split-operand (X3) variants use half-size
-  // stages so that two CTAs fit on an SM (<= ~113 KB of shared memory each)
-  static constexpr int kPy = X3 ? (C == 1 ? 2 : 1) : (C == 1 ? 4 : 2);
-  static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame
-  // A/W (MMA operand) ring: 2 stages for both modalities (a 3-stage depth
-  // ring measured the same 79.6 us per 8 x 720p launch and trips
-  // compute-sanitizer synccheck's mbarrier tracking)
+  // stages so that two CTAs fit on an SM (<= ~113 KB of shared memory each).
+  // F32 (float module API): a stage is 2 pixel rows of ONE channel (K = 32).
+  static constexpr int kPy = F32 ? 2 : X3 ? (C == 1 ? 2 : 1) : (C == 1 ? 4 : 2);
+  static constexpr int kSpt = 16 / kPy;                      // K stages per tubelet frame (u8)
   static constexpr int kNst = 2;
-  static constexpr uint32_t kU8_ = kTh * kPy * kTw * 16 * C;
+  static constexpr int kKst = F32 ? 32 : 16 * kPy * C;      // K per stage
+  static constexpr uint32_t kU8_ = F32 ? kTh * kPy * kTw * 16 * 4 : kTh * kPy * kTw * 16 * C;
   // raw-pixel TMA ring: the X3 variants fill the region the LN output (A2,
-  // 32 KB) needs anyway -- 5-8 stages in flight against HBM latency
-  static constexpr int kNu8 = X3 ? int(32768 / kU8_) : (C == 1 ? 4 : 3);
-  static constexpr uint32_t kU8 = kTh * kPy * kTw * 16 * C; // raw pixels per stage
-  static constexpr uint32_t kA = kRows * 16 * kPy * C * 2;  // fp16 A per stage
-  static constexpr uint32_t kW1 = 64 * 16 * kPy * C * 2;    // fp16 W per stage (one copy)
+  // 32 KB) needs anyway -- 5-8 stages in flight against HBM latency; the
+  // float boxes are 16 KB (2 or 3 stages)
+  static constexpr int kNu8 = F32 ? (X3 ? 2 : 3) : X3 ? int(32768 / kU8_) : (C == 1 ? 4 : 3);
+  static constexpr uint32_t kU8 = kU8_;                     // raw bytes per stage
+  static constexpr uint32_t kA1 = kRows * kKst * 2;         // fp16 A per stage, one copy
+  static constexpr uint32_t kA = F32 ? kA1 * kX : kA1;      // F32 X3: A_hi | A_lo
+  static constexpr uint32_t kW1 = 64 * kKst * 2;            // fp16 W per stage (one copy)
   static constexpr uint32_t kW = kW1 * kX;                  // [hi | lo]
   static constexpr uint32_t kQkvW1 = 192 * 64 * 2, kA21 = kRows * 64 * 2;
   static constexpr uint32_t kQkvW = kQkvW1 * kX, kA2 = kA21 * kX;
@@ -108,19 +109,25 @@ __device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint3
   lo = pack_bf16(x - h.x, y - h.y);
 }
 
-template <int C, bool X3>
+template <int C, bool X3, bool F32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
 embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tcw) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using S = EmbSmem<C, X3>;
+  using S = EmbSmem<C, X3, F32>;
   // pointer arithmetic (not integer casts) keeps the shared address space
   S& sm = *reinterpret_cast<S*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_w = (a.nw + kTw - 1) / kTw;
   const int ih0 = (blockIdx.x / tiles_w) * kTh, iw0 = (blockIdx.x % tiles_w) * kTw;
   const int it = blockIdx.y, b = blockIdx.z;
-  const int T = a.D.T, nst = T * S::kSpt;
+  const int T = a.D.T;
+  // F32: T x C x 8 image stages (2 rows of one channel of one sub-frame), then
+  // 8 mask-channel stages on the last slice (model.py:105-107: the mask channel
+  // is nonzero only in the stack's last frame)
+  const bool last_slice_cta = it == a.D.nt - 1;
+  const int nimg = F32 ? T * C * 8 : T * S::kSpt;
+  const int nst = nimg + (F32 && last_slice_cta ? 8 : 0);
 
   if (warp == 4 && lane == 0) {
     for (int i = 0; i < S::kNu8; ++i) {
@@ -139,7 +146,13 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     fence_mbar_init();
     tma_prefetch(&tm_u8);
   }
-  if (threadIdx.x < T) sm.slot[threadIdx.x] = a.frame_index[b * a.D.F + it * T + threadIdx.x];
+  if (!F32 && threadIdx.x < T) sm.slot[threadIdx.x] = a.frame_index[b * a.D.F + it * T + threadIdx.x];
+  if (F32 && threadIdx.x < T) {
+    // front padding (model.py:99-101): stack frame fr comes from input frame
+    // max(0, fr - (F - f_in))
+    const int fr = it * T + threadIdx.x, src = max(0, fr - (a.D.F - a.f_in));
+    sm.slot[threadIdx.x] = (b * a.f_in + src) * C;     // plane index of channel 0
+  }
   for (int i = threadIdx.x; i < 64; i += blockDim.x) {
     sm.par[i] = a.emb_b[i];
     sm.par[64 + i] = a.time_pos[it * 64 + i];
@@ -159,12 +172,19 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     if (lane == 0) {
       // raw pixels run up to S::kNu8 stages ahead: their slots free as soon as
       // the converters have read them
-      for (int st = 0; st < nst; ++st) {
+      for (int st = 0; st < nimg; ++st) {
         const int pu = st % S::kNu8;
         mbar_wait(&sm.u8_empty[pu], ((st / S::kNu8) & 1) ^ 1);
         mbar_expect_tx(&sm.u8_full[pu], S::kU8);
-        tma_load_5d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], 0, iw0, S::kPy * (st % S::kSpt), ih0,
-                    sm.slot[st / S::kSpt]);
+        if constexpr (F32) {
+          // (256 px, 2 rows, 8 patch rows) of plane (b, frame, ch)
+          const int tt = st / (C * 8), ch = (st / 8) % C, rp = st % 8;
+          tma_load_4d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], iw0 * 16, 2 * rp, ih0,
+                      sm.slot[tt] + ch);
+        } else {
+          tma_load_5d(sm.u8(pu), &tm_u8, &sm.u8_full[pu], 0, iw0, S::kPy * (st % S::kSpt), ih0,
+                      sm.slot[st / S::kSpt]);
+        }
       }
     } else if (lane == 1) {
       // weights follow the MMA-operand ring (independent thread, own waits)
@@ -175,7 +195,8 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         // the host packs 2-row stages back to back, so kPy/2 of them are one
         // block (X3: one [hi | lo] pair per kernel stage)
         const __half* src =
-            C == 2 ? (X3 ? tcw.emb16_3 + size_t(st) * (S::kW / 2) : tcw.emb16 + size_t(st) * (S::kW / 2))
+            F32 ? (X3 ? tcw.embf3 : tcw.embf) + size_t(st) * (S::kW / 2)
+            : C == 2 ? (X3 ? tcw.emb16_3 + size_t(st) * (S::kW / 2) : tcw.emb16 + size_t(st) * (S::kW / 2))
                    : (X3 ? tcw.emb3 + size_t(st) * (S::kW / 2)
                          : tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems);
         bulk_load(sm.w[ps], src, S::kW, &sm.w_full[ps]);
@@ -196,11 +217,14 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         tc_fence_after();
         const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w[ps]);
 #pragma unroll
-        for (int kk = 0; kk < S::kPy * C; ++kk) {
+        for (int kk = 0; kk < S::kKst / 16; ++kk) {
           const uint64_t ad = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
           mma_ss(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
           if (X3)   // pixels are exact: pix . W_lo completes the product
             mma_ss(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+          if (F32 && X3)   // float inputs: + x_lo . W_hi
+            mma_ss(tmem, sdesc(ab + S::kA1 + kk * 4096, 128, kSwizzleNone, 2048),
+                   sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
         }
         mma_commit(&sm.empty[ps]);
       }
@@ -231,9 +255,70 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     const int ih = ih0 + ihl, iw = iw0 + iwl;
     const bool valid = ih < a.nh && iw < a.nw;
     const int s = valid ? ih * a.nw + iw : 0;
-    const bool masked = valid && a.rank[b * a.ns + s] >= 0;
+    const bool masked = !F32 && valid && a.rank[b * a.ns + s] >= 0;
     const bool last_slice = it == a.D.nt - 1;
-    for (int st = 0; st < nst; ++st) {
+    if constexpr (F32) {
+      // float module API: stage = 2 pixel rows of one channel; the corrupted
+      // (last) frame is multiplied by (1 - mask) (model.py:108-109); the mask
+      // channel is its own 8 stages (model.py:105-107)
+      const uint8_t* mrow = a.pmask + size_t(b) * a.h * a.w;
+      for (int st = 0; st < nst; ++st) {
+        const int ps = st % S::kNst, pu = st % S::kNu8;
+        const bool img = st < nimg;
+        if (img) mbar_wait(&sm.u8_full[pu], (st / S::kNu8) & 1);
+        if (st >= S::kNst) mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);
+        const int tt = img ? st / (C * 8) : T - 1, rp = img ? st % 8 : st - nimg;
+        const bool corrupted = last_slice && tt == T - 1;
+        uint8_t* arow = sm.a(ps) + m * 16;
+#pragma unroll
+        for (int pyl = 0; pyl < 2; ++pyl) {
+          const int y = ih * 16 + 2 * rp + pyl;
+          uint4 mk = make_uint4(0u, 0u, 0u, 0u);
+          if (valid && (corrupted || !img))
+            mk = __ldg(reinterpret_cast<const uint4*>(mrow + size_t(y) * a.w + iw * 16));
+          const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+          float v[16];
+          if (img) {
+            const float4* src = reinterpret_cast<const float4*>(
+                sm.u8(pu) + ((ihl * 2 + pyl) * 256 + iwl * 16) * 4);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 u = src[q];
+              v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+            }
+            if (corrupted) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if ((mw[e >> 2] >> (8 * (e & 3))) & 0xFFu) v[e] = 0.f;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = ((mw[e >> 2] >> (8 * (e & 3))) & 0xFFu) ? 1.f : 0.f;
+          }
+#pragma unroll
+          for (int kh = 0; kh < 2; ++kh) {             // K chunk pyl * 2 + kh: 8 pixels
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              hi[j] = pack_h2(v[8 * kh + 2 * j], v[8 * kh + 2 * j + 1]);
+              if (X3) {
+                const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[j]));
+                lo[j] = pack_h2(v[8 * kh + 2 * j] - hf.x, v[8 * kh + 2 * j + 1] - hf.y);
+              }
+            }
+            const int ki = pyl * 2 + kh;
+            *reinterpret_cast<uint4*>(arow + ki * 2048) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            if (X3)
+              *reinterpret_cast<uint4*>(arow + S::kA1 + ki * 2048) =
+                  make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+        }
+        if (img) mbar_arrive(&sm.u8_empty[pu]);
+        fence_proxy_async();
+        mbar_arrive(&sm.aready[ps]);
+      }
+    }
+    for (int st = 0; !F32 && st < nst; ++st) {
       const int ps = st % S::kNst, pu = st % S::kNu8;
       mbar_wait(&sm.u8_full[pu], (st / S::kNu8) & 1);
       if (st >= S::kNst) mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);   // A slot drained
@@ -275,11 +360,13 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         for (int j = 0; j < 32; ++j) x[32 * h + j] = __uint_as_float(r[j]);
       }
     }
-    const bool mterm = last_slice && masked;
+    const bool mterm = !F32 && last_slice && masked;   // F32: the mask channel is in the GEMM
     // (X3: the weights were scaled by 2^s; 2^-s / 255 is exactly 2^-s fl(1/255));
-    // u16 depth (C == 2: byte pairs, hi-byte weights x 256) is / 65535
-    const float pix_inv = C == 2 ? 1.f / 65535.f : 1.f / 255.f;
-    const float inv255 = X3 ? (C == 2 ? tcw.sc_emb16 : tcw.sc_emb) * pix_inv : pix_inv;
+    // u16 depth (C == 2: byte pairs, hi-byte weights x 256) is / 65535; float
+    // stacks are already in [0, 1]
+    const float pix_inv = F32 ? 1.f : C == 2 ? 1.f / 65535.f : 1.f / 255.f;
+    const float inv255 =
+        X3 ? (F32 ? tcw.sc_embf : C == 2 ? tcw.sc_emb16 : tcw.sc_emb) * pix_inv : pix_inv;
 #pragma unroll
     for (int o = 0; o < 64; ++o) {
       float v = fmaf(x[o], inv255, sm.par[o]);
@@ -437,7 +524,35 @@ bool embed_tc_supported(const Dims& D) {
   return D.p == 16 && D.d == 64 && D.heads == 2 && (D.c == 1 || D.c == 3) && D.T <= 2;
 }
 
+// float module API: stack (b, f_in, c, h, w) planes viewed as (w, 16 rows,
+// h/16 patch rows, plane) with boxes of (256 px, 2 rows, 8 patch rows)
+template <int C, bool X3>
+cudaError_t launch_f32(const EmbedTcArgs& a, cudaStream_t s) {
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  CUtensorMap tm;
+  cuuint64_t dims[4] = {cuuint64_t(a.w), 16, cuuint64_t(a.nh), cuuint64_t(a.b) * a.f_in * C};
+  cuuint64_t strides[3] = {cuuint64_t(a.w) * 4, cuuint64_t(16) * a.w * 4,
+                           cuuint64_t(a.h) * a.w * 4};
+  cuuint32_t box[4] = {cuuint32_t(kTw * 16), 2, kTh, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(a.stack), dims, strides,
+         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const size_t smem = sizeof(EmbSmem<C, X3, true>) + 128;
+  if (cudaError_t e = smem_optin(embed_tc_kernel<C, X3, true>, int(smem))) return e;
+  const int tiles = ((a.nh + kTh - 1) / kTh) * ((a.nw + kTw - 1) / kTw);
+  launch_seq(embed_tc_kernel<C, X3, true>, dim3(tiles, a.D.nt, a.b), kThreads, smem, s, tm, a,
+             *a.tcw);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s) {
+  if (a.f32) {
+    if (a.x3) return a.D.c == 3 ? launch_f32<3, true>(a, s) : launch_f32<1, true>(a, s);
+    return a.D.c == 3 ? launch_f32<3, false>(a, s) : launch_f32<1, false>(a, s);
+  }
   // 16-bit depth: the u16 plane is read as byte pairs (lo, hi), i.e. a
   // two-"channel" u8 image whose hi-byte weights carry the factor 256
   if (a.u16) return a.x3 ? launch_c<2, true>(a, s) : launch_c<2, false>(a, s);

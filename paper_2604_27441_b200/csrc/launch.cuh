@@ -84,6 +84,11 @@ struct EmbedTcArgs {
   int b, h, w, nh, nw, ns, ns_pad;
   int x3;                         // precise: split operands (TcW emb3/qkv0_3), fp32 x
   int u16;                        // frames are u16 depth planes (TcW emb16 / emb16_3)
+  // or: the float module API (TcW embf / embf3): stack (b, f_in, c, h, w) in
+  // [0, 1] (front-padded to F frames on the fly), pixel mask (b, h, w)
+  int f32;
+  const float* stack; int f_in;
+  const uint8_t* pmask;
 };
 cudaError_t launch_embed_tc(const EmbedTcArgs& a, cudaStream_t s);
 

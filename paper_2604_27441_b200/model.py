@@ -126,6 +126,9 @@ class MaskedVideoModel(nn.Module):
         dev = nat.device
         with torch.cuda.device(dev):
             st = stack.detach().to(dev, torch.float32).contiguous()
-            mk = mask.detach().to(dev).to(torch.uint8).contiguous()
+            mk = mask.detach().to(dev)
+            # bool and uint8 share the byte layout (nonzero = corrupted): no copy
+            mk = (mk.view(torch.uint8) if mk.dtype == torch.bool else
+                  mk if mk.dtype == torch.uint8 else (mk != 0).to(torch.uint8)).contiguous()
             out = nat.forward_f32(st, mk, _native.precision_code(self.precision))
         return out if stack.is_cuda else out.to(stack.device)
