@@ -221,6 +221,8 @@ def test_fast_path_runs_tensor_core_attention():
     # block + head on tcgen05 (k_last_tc.cu)
     assert prof.launches["attn_tc"] == 4 and prof.launches["attn_simt"] == 0
     assert prof.launches["last_tc"] == 1
+    # the float stack embeds on tcgen05 too (embed_tc F32; no ln_qkv kernel)
+    assert prof.launches["embed"] == 1 and prof.launches["ln_qkv"] == 0
     m.precision = "precise"
     with _native.StageProfile() as prof:
         m(s, mk)
@@ -331,3 +333,25 @@ def test_recover_720p_20pct_vs_oracle(c):
         assert d.max() <= LSB[prec], (prec, d.max())
         ds = abs(ssim(frames[-1], got) - ssim(frames[-1], want))
         assert ds <= SSIM_TOL, (prec, ds)
+
+
+def test_f32_embed_tc_equals_simt(tmp_path):
+    """The float module API's tcgen05 embedding (float planes by TMA, pixel
+    mask zeroing + mask channel as extra K stages) against the fp32 CUDA-core
+    embedding (NVREC_F32_EMBED_SIMT=1) on the same inputs: float outputs of
+    both precisions and modalities within 5e-6 (precise; each is within 1.5e-5
+    of the reference) / 1e-3 (fast)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    res = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / ("f%s.npz" % flag))
+        subprocess.run([sys.executable, os.path.join(here, "last_block_probe.py"), path],
+                       check=True, env=dict(os.environ, NVREC_F32_EMBED_SIMT=flag), timeout=300)
+        res[flag] = np.load(path)
+    for c in (3, 1):
+        for prec, tol in (("fast", 1e-3), ("precise", 5e-6)):
+            key = "f32_%d_%s" % (c, prec)
+            e = np.abs(res["0"][key] - res["1"][key]).max()
+            assert e <= tol, (key, e)
