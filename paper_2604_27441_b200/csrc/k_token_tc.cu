@@ -99,14 +99,12 @@ token_tc_kernel(TokenTcArgs a) {
     bulk_load(sm.w + kOffQkvS, a.w_qkv_next, 12288 * 2, &sm.bar_w);
   }
   {
-    const struct { const float* src; int off, n; } vecs[12] = {
-        {a.b_proj_s, kPBProjS, 64}, {a.ln_t_w, kPLnTw, 64}, {a.ln_t_b, kPLnTb, 64},
-        {a.b_qkv_t, kPBQkvT, 192}, {a.b_proj_t, kPBProjT, 64}, {a.ln_m_w, kPLnMw, 64},
-        {a.ln_m_b, kPLnMb, 64}, {a.b_fc1, kPBFc1, 256}, {a.b_fc2, kPBFc2, 64},
-        {a.ln_s_next_w, kPLnSw, 64}, {a.ln_s_next_b, kPLnSb, 64}, {a.b_qkv_next, kPBQkvN, 192}};
-#pragma unroll 1
-    for (int v = 0; v < 12; ++v)
-      for (int i = threadIdx.x; i < vecs[v].n; i += blockDim.x) sm.par[vecs[v].off + i] = vecs[v].src[i];
+    const float* const src[12] = {a.b_proj_s, a.ln_t_w, a.ln_t_b, a.b_qkv_t, a.b_proj_t,
+                                  a.ln_m_w, a.ln_m_b, a.b_fc1, a.b_fc2, a.ln_s_next_w,
+                                  a.ln_s_next_b, a.b_qkv_next};
+    static_assert(kPBProjS == 0 && kPLnTw == 64 && kPBQkvT == 192 && kPBFc1 == 576 &&
+                  kPBQkvN == 1024 && kParFloats == 1216, "par layout == tail_par_end");
+    stage_tail_params<kThreads>(sm.par, src);
   }
   if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
   tc_fence_before();

@@ -221,4 +221,41 @@ __device__ __forceinline__ float gelu_as(float v) {
   return v * (v >= 0.f ? 1.f - h : h);
 }
 
+// Stage the 12 block-tail parameter vectors (biases and LayerNorm affines,
+// concatenated in `par` order, vector q ending at tail_par_end(q)) into shared
+// memory with every global load in flight at once: one flat, unrolled pass
+// (a struct-array loop indexed at run time lands in local memory and
+// serialises twelve load round trips at every CTA start).
+__host__ __device__ constexpr int tail_par_end(int q) {
+  return q < 3 ? 64 * (q + 1) : q == 3 ? 384 : q < 7 ? 448 + 64 * (q - 4) : q == 7 ? 832
+       : 896 + 64 * (q - 8) > 1024 ? 1216 : 896 + 64 * (q - 8);
+}
+static_assert(tail_par_end(0) == 64 && tail_par_end(3) == 384 && tail_par_end(6) == 576 &&
+              tail_par_end(7) == 832 && tail_par_end(10) == 1024 && tail_par_end(11) == 1216,
+              "tail parameter layout");
+template <int kThreadsT>
+__device__ __forceinline__ void stage_tail_params(float* par, const float* const (&src)[12]) {
+  constexpr int kN = tail_par_end(11);
+  constexpr int kPer = (kN + kThreadsT - 1) / kThreadsT;
+  float v[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = int(threadIdx.x) + k * kThreadsT;
+    const float* p = src[11];
+    int base = tail_par_end(10);
+#pragma unroll
+    for (int q = 10; q >= 0; --q)
+      if (i < tail_par_end(q)) {
+        p = src[q];
+        base = q ? tail_par_end(q - 1) : 0;
+      }
+    v[k] = i < kN ? __ldg(p + (i - base)) : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = int(threadIdx.x) + k * kThreadsT;
+    if (i < kN) par[i] = v[k];
+  }
+}
+
 }  // namespace nvrec

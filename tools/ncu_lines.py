@@ -1,6 +1,6 @@
 """Aggregate an ncu report's warp-stall samples by CUDA source line.
 
-    python tools/ncu_lines.py REPORT.ncu-rep OBJECT.o [top]
+    python tools/ncu_lines.py REPORT.ncu-rep OBJECT.o [top] [kernel-regex] [sass-function-substring]
 
 OBJECT.o is the -lineinfo object the kernel came from (its SASS offsets carry
 the file:line table; they match the report's addresses relative to the
@@ -14,15 +14,20 @@ import sys
 import tempfile
 
 
-def main(rep, obj, top=25):
+def main(rep, obj, top=25, kre=None, fsub=None):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, check=True,
                    capture_output=True)
     cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
     sass = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, cubin)], capture_output=True,
                           text=True).stdout.splitlines()
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    # kernel-regex[@skip]: the skip-th launch matching the regex
+    flt = []
+    if kre:
+        name, _, skip = kre.partition("@")
+        flt = ["--kernel-name", "regex:" + name, "--launch-skip", skip or "0", "--launch-count", "1"]
+    out = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source",
+                          "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, data = rows[1], rows[2:]
     ai = hdr.index("Warp Stall Sampling (All Samples)")
@@ -41,20 +46,29 @@ def main(rep, obj, top=25):
         m2 = re.match(r'\s+/\*([0-9a-f]{4,})\*/', line)
         if m2 and cur and cur_fn:
             funcs[cur_fn][int(m2.group(1), 16)] = cur
-    cands = [f for f in funcs if kname in f] or list(funcs)
+    cands = [f for f in funcs if kname in f and (not fsub or fsub in f)] or list(funcs)
     base = int(data[0][0], 16)
-    tot = sum(float(r[ai]) for r in data if len(r) > ai) or 1.0
+    def fl(x):
+        try:
+            return float(x)
+        except ValueError:
+            return 0.0
+    tot = sum(fl(r[ai]) for r in data if len(r) > ai) or 1.0
     for fn in cands:
         agg = {}
         for r in data:
             if len(r) <= ai:
                 continue
-            key = funcs[fn].get(int(r[0], 16) - base, ("?", 0))
-            agg[key] = agg.get(key, 0.0) + float(r[ai])
+            try:
+                key = funcs[fn].get(int(r[0], 16) - base, ("?", 0))
+            except ValueError:
+                continue
+            agg[key] = agg.get(key, 0.0) + fl(r[ai])
         print("==", fn)
         for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
             print("%5.1f%% %s:%d" % (100 * v / tot, k[0], k[1]))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25,
+         sys.argv[4] if len(sys.argv) > 4 else None, sys.argv[5] if len(sys.argv) > 5 else None)
