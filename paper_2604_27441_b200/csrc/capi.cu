@@ -1080,6 +1080,7 @@ int nvrec_baseline_u8(int32_t depth, int32_t b, int32_t h, int32_t w, int32_t c,
 int nvrec_debug_attn_trace(unsigned long long* host, int n) { return nvrec::attn_trace(host, n); }
 int nvrec_debug_last_trace(unsigned long long* host, int n) { return nvrec::last_trace(host, n); }
 int nvrec_debug_token_x3_trace(unsigned long long* host, int n) { return nvrec::token_x3_trace(host, n); }
+int nvrec_debug_embed_trace(unsigned long long* host, int n) { return nvrec::embed_trace(host, n); }
 #endif
 
 int64_t nvrec_attn_fixup_items(void) {

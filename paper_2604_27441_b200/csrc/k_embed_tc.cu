@@ -76,19 +76,37 @@ struct __align__(128) EmbSmem {
   static constexpr uint32_t kW = kW1 * kX;                  // [hi | lo]
   static constexpr uint32_t kQkvW1 = 192 * 64 * 2, kA21 = kRows * 64 * 2;
   static constexpr uint32_t kQkvW = kQkvW1 * kX, kA2 = kA21 * kX;
-  static constexpr uint32_t kARegion = kNst * kA > kQkvW ? kNst * kA : kQkvW;
+  // Weight ring.  The per-stage weight blocks come from L2 and bound the K
+  // loop when only two are in flight (measured: the MMA waited ~600 clk per
+  // stage); the u8 split variants keep four in flight and park the qkv
+  // weights in the weight region after the K loop (the A ring shrinks to two
+  // stages), which still fits two CTAs per SM.
+  static constexpr bool kQkvInW = X3 && !F32;
+  static constexpr int kNw = kQkvInW ? 4 : kNst;
+  static constexpr uint32_t kWRegion = kQkvInW && kNw * kW < kQkvW ? kQkvW : kNw * kW;
+  static constexpr uint32_t kARegion =
+      kQkvInW ? kNst * kA : (kNst * kA > kQkvW ? kNst * kA : kQkvW);
   static constexpr uint32_t kURegion = kNu8 * kU8 > kA2 ? kNu8 * kU8 : kA2;
-  uint8_t a_raw[kARegion];        // A ring, then: qkv weights [192 x 64] fp16
-  uint8_t w[kNst][kW];
-  uint8_t u8_raw[kURegion];       // pixel ring, then: LN output (A2) [128 x 64] fp16
+  uint8_t a_raw[kARegion];        // A ring (then the qkv weights unless kQkvInW)
+  uint8_t w_raw[kWRegion];        // weight ring (then the qkv weights if kQkvInW)
+  uint8_t u8_raw[kURegion];       // pixel ring, then: LN output (A2) [128 x 64] fp16, then V^T staging
   float par[64 * 5 + 192];        // bias | time_pos[it] | wmsum | ln_w | ln_b | qkv_b
-  uint64_t u8_full[kNu8], u8_empty[kNu8], w_full[kNst], aready[kNst], empty[kNst];
+  uint64_t u8_full[kNu8], u8_empty[kNu8], w_full[kNw], w_empty[kNw], aready[kNst], empty[kNst];
   uint64_t acc_full, wq_full, a2_ready, qkv_full;
   uint32_t tmem_base;
   int slot[16];
   __device__ uint8_t* a(int i) { return a_raw + i * kA; }
+  __device__ uint8_t* w(int i) { return w_raw + i * kW; }
+  __device__ uint8_t* qkvw() { return kQkvInW ? w_raw : a_raw; }
   __device__ uint8_t* u8(int i) { return u8_raw + i * kU8; }
 };
+
+// two CTAs per SM (<= 113.5 KB each incl. alignment slack and the 1 KB the
+// runtime reserves per CTA) for every u8 / u16 variant and the split float one
+static_assert(sizeof(EmbSmem<3, true>) + 128 <= 112 * 1024, "RGB X3 embed: two CTAs per SM");
+static_assert(sizeof(EmbSmem<1, true>) + 128 <= 112 * 1024, "depth X3 embed: two CTAs per SM");
+static_assert(sizeof(EmbSmem<2, true>) + 128 <= 112 * 1024, "u16 X3 embed: two CTAs per SM");
+static_assert(sizeof(EmbSmem<3, false>) + 128 <= 112 * 1024, "RGB embed: two CTAs per SM");
 
 __device__ __forceinline__ uint32_t u8x2_to_h2(uint32_t w, uint32_t sel) {
   uint32_t p = __byte_perm(w, 0x64646464u, sel);     // fp16 1024 + byte
@@ -108,6 +126,20 @@ __device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint3
   const float2 h = unpack_bf16(hi);
   lo = pack_bf16(x - h.x, y - h.y);
 }
+
+#ifdef NVREC_TRACE
+// CTA 0: MMA-thread timestamps per stage (0: start, 1: A ready, 2: W ready) and
+// converter-warp-0 lane-0 timestamps (3: pixels ready), tools/trace_embed.py
+__device__ unsigned long long g_emb_trace[64][4];
+__device__ unsigned long long g_emb_trace_end[8];
+#define ET(st, e) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (st) < 64) g_emb_trace[st][e] = clock64(); } while (0)
+#define EE(i) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) g_emb_trace_end[i] = clock64(); } while (0)
+#else
+#define ET(st, e) do {} while (0)
+#define EE(i) do {} while (0)
+#endif
 
 template <int C, bool X3, bool F32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -135,9 +167,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       mbar_init(&sm.u8_empty[i], 128);
     }
     for (int i = 0; i < S::kNst; ++i) {
-      mbar_init(&sm.w_full[i], 1);
       mbar_init(&sm.aready[i], 128);
       mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < S::kNw; ++i) {
+      mbar_init(&sm.w_full[i], 1);
+      mbar_init(&sm.w_empty[i], 1);
     }
     mbar_init(&sm.acc_full, 1);
     mbar_init(&sm.wq_full, 1);
@@ -187,10 +222,10 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         }
       }
     } else if (lane == 1) {
-      // weights follow the MMA-operand ring (independent thread, own waits)
+      // weights: their own ring of kNw stages (independent thread, own waits)
       for (int st = 0; st < nst; ++st) {
-        const int ps = st % S::kNst;
-        mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);
+        const int ps = st % S::kNw;
+        mbar_wait(&sm.w_empty[ps], ((st / S::kNw) & 1) ^ 1);
         mbar_expect_tx(&sm.w_full[ps], S::kW);
         // the host packs 2-row stages back to back, so kPy/2 of them are one
         // block (X3: one [hi | lo] pair per kernel stage)
@@ -199,23 +234,26 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
             : C == 2 ? (X3 ? tcw.emb16_3 + size_t(st) * (S::kW / 2) : tcw.emb16 + size_t(st) * (S::kW / 2))
                    : (X3 ? tcw.emb3 + size_t(st) * (S::kW / 2)
                          : tcw.emb + size_t(st) * (S::kPy / 2) * tcw.emb_stage_elems);
-        bulk_load(sm.w[ps], src, S::kW, &sm.w_full[ps]);
+        bulk_load(sm.w(ps), src, S::kW, &sm.w_full[ps]);
       }
-      // qkv weights into the A ring once the last embed MMA has read it
+      // qkv weights into the A ring / weight ring once the last embed MMA has read it
       mbar_wait(&sm.acc_full, 0);
       mbar_expect_tx(&sm.wq_full, S::kQkvW);
-      bulk_load(sm.a(0), X3 ? tcw.qkv0_3 : tcw.qkv0, S::kQkvW, &sm.wq_full);
+      bulk_load(sm.qkvw(), X3 ? tcw.qkv0_3 : tcw.qkv0, S::kQkvW, &sm.wq_full);
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA
     if (lane == 0) {
       const uint32_t idesc = idesc_f16(128, 64);
       for (int st = 0; st < nst; ++st) {
-        const int ps = st % S::kNst;
+        const int ps = st % S::kNst, pw = st % S::kNw;
+        ET(st, 0);
         mbar_wait(&sm.aready[ps], (st / S::kNst) & 1);
-        mbar_wait(&sm.w_full[ps], (st / S::kNst) & 1);
+        ET(st, 1);
+        mbar_wait(&sm.w_full[pw], (st / S::kNw) & 1);
+        ET(st, 2);
         tc_fence_after();
-        const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w[ps]);
+        const uint32_t ab = smem_u32(sm.a(ps)), wb = smem_u32(sm.w(pw));
 #pragma unroll
         for (int kk = 0; kk < S::kKst / 16; ++kk) {
           const uint64_t ad = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
@@ -227,13 +265,14 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
                    sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
         }
         mma_commit(&sm.empty[ps]);
+        mma_commit(&sm.w_empty[pw]);
       }
       mma_commit(&sm.acc_full);
       mbar_wait(&sm.wq_full, 0);
       mbar_wait(&sm.a2_ready, 0);
       tc_fence_after();
       const uint32_t idesc2 = idesc_f16(128, 192);
-      const uint32_t a2b = smem_u32(sm.u8(0)), wqb = smem_u32(sm.a(0));
+      const uint32_t a2b = smem_u32(sm.u8(0)), wqb = smem_u32(sm.qkvw());
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t yh = sdesc(a2b + kk * 4096, 128, kSwizzleNone, 2048);
@@ -321,6 +360,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     for (int st = 0; !F32 && st < nst; ++st) {
       const int ps = st % S::kNst, pu = st % S::kNu8;
       mbar_wait(&sm.u8_full[pu], (st / S::kNu8) & 1);
+      if (threadIdx.x == 0) ET(st, 3);
       if (st >= S::kNst) mbar_wait(&sm.empty[ps], ((st / S::kNst) & 1) ^ 1);   // A slot drained
       const bool zero = last_slice && (st / S::kSpt) == T - 1 && masked;   // corrupted frame
       uint8_t* arow = sm.a(ps) + m * 16;
@@ -347,7 +387,9 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     }
     // ---- epilogue 1: x = acc/255 + bias + time_pos (+ mask term) ------------
     const uint32_t lane_off = uint32_t(warp * 32) << 16;
+    EE(0);
     mbar_wait(&sm.acc_full, 0);
+    EE(1);
     tc_fence_after();
     float x[64];
     {
@@ -418,8 +460,14 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     }
     fence_proxy_async();
     mbar_arrive(&sm.a2_ready);
+    EE(2);
     // ---- epilogue 2: q, k, v (+ bias) -> bf16 attention operands -----------
+    // V^T staging over the LN output (A2), which the finished qkv MMA has read
+    constexpr int kVtR = X3 ? 64 : 32;                 // V^T rows per head
+    __nv_bfloat16* vst = reinterpret_cast<__nv_bfloat16*>(sm.u8(0));
+    static_assert(2 * kVtR * kRows * 2 <= S::kURegion, "V^T staging fits the A2 region");
     mbar_wait(&sm.qkv_full, 0);
+    EE(3);
     tc_fence_after();
     int qrow = s;
     if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
@@ -450,12 +498,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
             d4[4 + e / 8] = make_uint4(l[0], l[1], l[2], l[3]);
           }
         } else {
-          __nv_bfloat16* dst = a.vth + seq * 64 * a.ns_pad + s;
+          // V^T rows e (hi) and 32 + e (lo), staged per token (coalesced below)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const __nv_bfloat16 h = __float2bfloat16_rn(v[e]);
-            dst[size_t(e) * a.ns_pad] = h;
-            dst[size_t(32 + e) * a.ns_pad] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
+            vst[(head * kVtR + e) * kRows + m] = h;
+            vst[(head * kVtR + 32 + e) * kRows + m] = __float2bfloat16_rn(v[e] - __bfloat162float(h));
           }
         }
         continue;
@@ -470,17 +518,47 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
           d4[e / 8] = make_uint4(pack_bf16(v[e], v[e + 1]), pack_bf16(v[e + 2], v[e + 3]),
                                  pack_bf16(v[e + 4], v[e + 5]), pack_bf16(v[e + 6], v[e + 7]));
       } else {
-        __nv_bfloat16* dst = a.vth + seq * 32 * a.ns_pad + s;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) dst[size_t(e) * a.ns_pad] = __float2bfloat16_rn(v[e]);
+        for (int e = 0; e < 32; ++e) vst[(head * kVtR + e) * kRows + m] = __float2bfloat16_rn(v[e]);
+      }
+    }
+    // V^T: the tile's 8 patch rows of 16 positions per (head, row), 16 bytes
+    // (8 positions) per store instead of one 2-byte store per element
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    for (int idx = m; idx < 2 * kVtR * 16; idx += kRows) {
+      const int half = idx & 1, r = (idx >> 1) & 7, row = idx >> 4;   // row = head * kVtR + e
+      const int head = row / kVtR, e = row - head * kVtR;
+      const int ihr = ih0 + r, iwc = iw0 + 8 * half;
+      if (ihr >= a.nh || iwc >= a.nw) continue;
+      const int s0 = ihr * a.nw + iwc;
+      const size_t seq = size_t(b * a.D.nt + it) * 2 + head;
+      __nv_bfloat16* dst = a.vth + (seq * kVtR + e) * a.ns_pad + s0;
+      const __nv_bfloat16* src = vst + row * kRows + r * 16 + 8 * half;
+      if (iwc + 8 <= a.nw && (s0 & 7) == 0) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      } else {
+        for (int k = 0; k < 8 && iwc + k < a.nw; ++k) dst[k] = src[k];
       }
     }
   }
+  EE(4);
   tc_fence_before();
   __syncthreads();
+  EE(5);
   if (warp == 0) tmem_dealloc<256>(tmem);
   pdl_trigger();
 }
+
+#ifdef NVREC_TRACE
+}  // namespace
+int embed_trace(unsigned long long* host, int n) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(host, g_emb_trace, 64 * 4 * 8) != cudaSuccess) return -1;
+  if (n > 256 && cudaMemcpyFromSymbol(host + 256, g_emb_trace_end, 8 * 8) != cudaSuccess) return -1;
+  return n;
+}
+namespace {
+#endif
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

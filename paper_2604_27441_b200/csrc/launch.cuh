@@ -168,6 +168,7 @@ int64_t attn_fixup_items();   // -1 on a CUDA error
 int attn_trace(unsigned long long* host, int n);   // trace build (tools/trace_attn.py)
 int last_trace(unsigned long long* host, int n);   // trace build (tools/trace_last.py)
 int token_x3_trace(unsigned long long* host, int n);   // trace build (tools/trace_token.py)
+int embed_trace(unsigned long long* host, int n);      // trace build (tools/trace_embed.py)
 #endif
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,
