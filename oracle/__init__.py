@@ -16,12 +16,18 @@ Modules
                    plain state dict, in fp32 torch-CPU ops -- the same ATen
                    kernels the reference calls.
 ``recover``        restatement of ``RecoveryServer._recover``
-                   (``pkg/nvrec/src/nvrec/server.py:181-196``).
+                   (``pkg/nvrec/src/nvrec/server.py:181-196``) and its 16-bit
+                   depth extension ``recover16`` (65535 in place of 255).
 ``lossmask``       restatement of the loss-mask construction:
                    ``Receiver._finalize_p`` zero-fill (``receiver.py:224-237``),
                    ``codec.parse_header``/``block_ranges``/``_corrupted_blocks``
                    /``decode`` mask assembly (``codec.py:159-201,250-320``) and
                    the wire bitset (``recovery.py:214-227``).
+``codec``          ``codec.decode`` / ``decode_bytes`` zero-fill decode and
+                   ``fec.rs_reconstruct`` (``codec.py:260-340``, ``fec.py:144-163``).
+``baseline``       ``recover_baseline_rgb/_depth`` (``recovery.py:94-196``).
+``metrics``        the SSIM of ``rgbdstream/metrics.py:41-72`` (north_star's
+                   |dSSIM| <= 1e-3 bar).
 
 Pinning
 -------
