@@ -238,7 +238,93 @@ void run(const char* name, int warps, double bytes_per_cta) {
   cudaFree(sink);
 }
 
+
+// mode R: the dense precise attention's MMA stream with the kernel's operand
+// addresses: Q of 2 query tiles (16 KB each), K/V in a 4-stage ring (16 KB +
+// 16 KB per key tile, key tile j = n / 2), S buffers n % 3, O' per tile.  rot = 0
+// reuses stage 0 every time (operands possibly cached), rot = 1 rotates.
+__global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int rot, int qtmem) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bar;
+  uint8_t* base = dsm + ((1024 - (smem_u32(dsm) & 1023)) & 1023);
+  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tbase);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t t = tbase;
+  unsigned long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    const uint32_t q0 = smem_u32(base), k0 = q0 + 32768, v0 = k0 + 4 * 16384;
+    constexpr uint32_t idS = idesc_bf16(128, 128), idP64 = idesc_bf16(128, 64),
+                       idP32 = idesc_bf16(128, 32);
+    constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
+    for (int n = 0; n < 2048; ++n) {
+      const int tq = n & 1, j = n >> 1, st = rot ? (j & 3) : 0;
+      const uint32_t sc = t + (n % 3) * 128;
+      const uint32_t qb = q0 + tq * 16384, kb = k0 + st * 16384;
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        if (qtmem)   // A (Q) from TMEM columns of the O' area (timing only)
+          mma_ts(sc, t + 384 + 8 * (u & 3), sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
+        else
+          mma_ss(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
+                 sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
+      }
+      if (n >= 2) {
+        const int m = n - 2, jm = m >> 1, sv = rot ? (jm & 3) : 0;
+        const uint32_t bc = t + (m % 3) * 128, oc = t + 384 + 64 * (m & 1);
+        const uint32_t vb = v0 + sv * 16384;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
+          const uint32_t vh = vb + (kk >> 2) * 8192 + (kk & 3) * 32;
+          mma_ts(oc, ah, sdesc(vh, 1024, kSwizzle128B), idP64, kk);
+          mma_ts(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), idP32, 1);
+        }
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+  }
+  __syncthreads();
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(t);
+}
+
+void run_rot(int rot, int qtmem) {
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, 148 * 8);
+  const int smem = 160 * 1024 + 1024;
+  cudaFuncSetAttribute(rot_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  rot_bench<<<148, 128, smem>>>(cyc, rot, qtmem);
+  cudaDeviceSynchronize();
+  rot_bench<<<148, 128, smem>>>(cyc, rot, qtmem);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
+  double mean = 0;
+  for (int i = 0; i < 148; ++i) mean += double(h[i]) / 148;
+  printf("x3w MMA stream, kernel operand layout, rotate=%d Q-in-TMEM=%d: %.1f clk/S tile (%s)\n",
+         rot, qtmem, mean / 2048.0, cudaGetErrorString(e));
+  cudaFree(cyc);
+}
+
 int main() {
+  run_rot(0, 0);
+  run_rot(1, 0);
+  run_rot(1, 1);
+  return 0;
   for (int w : {1, 2, 4, 8, 16}) {
     const double bytes = double(w) * kIters * 4 * 32 * 32 * 4;   // warps x iters x 4 x (32 lanes x 32 cols x 4 B)
     run<0>("tcgen05.ld 32x32b.x32", w, bytes);
