@@ -1081,6 +1081,7 @@ int nvrec_debug_attn_trace(unsigned long long* host, int n) { return nvrec::attn
 int nvrec_debug_last_trace(unsigned long long* host, int n) { return nvrec::last_trace(host, n); }
 int nvrec_debug_token_x3_trace(unsigned long long* host, int n) { return nvrec::token_x3_trace(host, n); }
 int nvrec_debug_embed_trace(unsigned long long* host, int n) { return nvrec::embed_trace(host, n); }
+int nvrec_debug_token_tc_trace(unsigned long long* host, int n) { return nvrec::token_tc_trace(host, n); }
 #endif
 
 int64_t nvrec_attn_fixup_items(void) {

@@ -502,10 +502,11 @@ last_tc_kernel(LastTcArgs a) {
         tmem_wait_ld();
         const float* bias = a.b_fc1 + 128 * H + 64 * gq + 32 * sub;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          split_h2(gelu_as(fmaf(__uint_as_float(rr[e]), s1, __ldg(bias + e))),
-                   gelu_as(fmaf(__uint_as_float(rr[e + 1]), s1, __ldg(bias + e + 1))),
-                   rr[e / 2], lo[e / 2]);
+        for (int e = 0; e < 32; e += 2) {
+          const float2 g = gelu_as2(make_float2(fmaf(__uint_as_float(rr[e]), s1, __ldg(bias + e)),
+                                                fmaf(__uint_as_float(rr[e + 1]), s1, __ldg(bias + e + 1))));
+          split_h2(g.x, g.y, rr[e / 2], lo[e / 2]);
+        }
         tc_fence_before();
         __syncthreads();
         tc_fence_after();

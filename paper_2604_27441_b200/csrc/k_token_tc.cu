@@ -76,6 +76,14 @@ __device__ __forceinline__ void layernorm64(const float* x, float* y, const floa
   for (int o = 0; o < 64; ++o) y[o] = (x[o] - mean) * rstd * g[o] + bt[o];
 }
 
+#ifdef NVREC_TRACE
+__device__ unsigned long long g_tc_trace[2][16];
+#define TT(i) \
+  do { if (blockIdx.x == 0 && threadIdx.x == 0 && ntile < 2) g_tc_trace[ntile][i] = clock64(); } while (0)
+#else
+#define TT(i) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1)
 token_tc_kernel(TokenTcArgs a) {
   pdl_wait();
@@ -157,7 +165,9 @@ token_tc_kernel(TokenTcArgs a) {
   };
   const float scale = rsqrtf(32.f);
 
-  for (int tile = blockIdx.x * kSlots + slot; tile < n_tiles; tile += gridDim.x * kSlots) {
+  int ntile = 0;
+  for (int tile = blockIdx.x * kSlots + slot; tile < n_tiles; tile += gridDim.x * kSlots, ++ntile) {
+    TT(0);
     const int b = tile / tiles_per_b;
     const int s = (tile - b * tiles_per_b) * P + wq * ppw + jl;
     const bool valid = row_live && s < a.ns;
@@ -194,12 +204,16 @@ token_tc_kernel(TokenTcArgs a) {
         }
       }
     }
+    TT(1);
     gemm_a(0, kOffProjS, 64);
+    TT(2);
     add64(x, 0, P_ + kPBProjS);
     // ---- 2. qkv_t(LN_t(x)); temporal attention by warp shuffles --------------
     layernorm64(x, y, P_ + kPLnTw, P_ + kPLnTb);
     put_row64(A, m, y);
+    TT(3);
     gemm_a(0, kOffQkvT, 192);
+    TT(4);
 #pragma unroll 1
     for (int hh = 0; hh < 2; ++hh) {
       float q[32], kk_[32], vv[32];
@@ -253,12 +267,16 @@ token_tc_kernel(TokenTcArgs a) {
                        pack_h2(q[8 * c4 + 4], q[8 * c4 + 5]), pack_h2(q[8 * c4 + 6], q[8 * c4 + 7]));
     }
     // ---- 3. x += proj_t(o) ---------------------------------------------------
+    TT(5);
     gemm_a(0, kOffProjT, 64);
+    TT(6);
     add64(x, 0, P_ + kPBProjT);
     // ---- 4. h = GELU(fc1(LN_m(x))), written back to TMEM as fp16 pairs -----
     layernorm64(x, y, P_ + kPLnMw, P_ + kPLnMb);
     put_row64(A, m, y);
+    TT(7);
     gemm_a(0, kOffFc1, 256);
+    TT(8);
 #pragma unroll 1
     for (int c8 = 0; c8 < 8; ++c8) {               // 8 chunks of 32 hidden units
       uint32_t r[32], pk[16];
@@ -266,11 +284,15 @@ token_tc_kernel(TokenTcArgs a) {
       tmem_wait_ld();
 #pragma unroll
       for (int e = 0; e < 32; e += 2)
-        pk[e / 2] = pack_h2(gelu_as(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e]),
-                            gelu_as(__uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
+      {
+        const float2 g = gelu_as2(make_float2(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e],
+                                              __uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
+        pk[e / 2] = pack_h2(g.x, g.y);
+      }
       tmem_st16(tbase + lane_off + 16 * c8, pk);   // columns [16 c8, 16 c8 + 16)
     }
     tmem_wait_st();
+    TT(9);
     // ---- 5. x += fc2(h) (A from TMEM columns [0,128)), store x ---------------
     run([&] {
       const uint32_t idesc = idesc_f16(128, 64), lbo_b = 8 * 128;
@@ -279,6 +301,7 @@ token_tc_kernel(TokenTcArgs a) {
         mma_ts(tbase + 128, tbase + kk * 8, sdesc(bbase + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b),
                idesc, kk != 0);
     });
+    TT(10);
     add64(x, 128, P_ + kPBFc2);
     int qrow = s;
     if (a.qrank) qrow = valid ? a.qrank[b * a.ns + s] : -1;
@@ -291,7 +314,9 @@ token_tc_kernel(TokenTcArgs a) {
     // ---- 6. next block's LN_s + qkv_s -> bf16 attention operands ----------------
     layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
     put_row64(A, m, y);
+    TT(11);
     gemm_a(0, kOffQkvS, 192);
+    TT(12);
     // V^T stores in 4-byte pairs: lanes of adjacent positions (same slice)
     // swap one value per dimension pair, so position pair (2i, 2i+1) of dims
     // (e, e+1) goes out as two 32-bit stores instead of four 16-bit ones
@@ -334,6 +359,7 @@ token_tc_kernel(TokenTcArgs a) {
       }
     }
     // every thread's TMEM reads precede the next tile's first MMA (run()'s barrier)
+    TT(15);
   }
   tc_fence_before();
   __syncthreads();
@@ -342,6 +368,14 @@ token_tc_kernel(TokenTcArgs a) {
 }
 
 }  // namespace
+
+#ifdef NVREC_TRACE
+int token_tc_trace(unsigned long long* host, int n) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int m = n < 32 ? n : 32;
+  return cudaMemcpyFromSymbol(host, g_tc_trace, m * 8) == cudaSuccess ? m : -1;
+}
+#endif
 
 bool token_tc_supported(const Dims& D) {
   return D.d == 64 && D.heads == 2 && D.nt <= 8 && D.hidden == 256;

@@ -287,9 +287,11 @@ token_x3_kernel(TokenX3Args a) {
           tmem_wait_ld();
           const float* bias = P_ + kPBFc1 + 128 * H + 64 * g;
 #pragma unroll
-          for (int e = 0; e < 64; e += 2)
-            split_h2(gelu_as(fmaf(__uint_as_float(r[e]), s1, bias[e])),
-                     gelu_as(fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])), r[e / 2], lo[e / 2]);
+          for (int e = 0; e < 64; e += 2) {
+            const float2 g = gelu_as2(make_float2(fmaf(__uint_as_float(r[e]), s1, bias[e]),
+                                                  fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])));
+            split_h2(g.x, g.y, r[e / 2], lo[e / 2]);
+          }
           tmem_st16(tbase + lane_off + 64 * g, r);
           tmem_st16(tbase + lane_off + 64 * g + 16, r + 16);
           tmem_st16(tbase + lane_off + 64 * g + 32, lo);

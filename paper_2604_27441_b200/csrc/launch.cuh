@@ -169,6 +169,7 @@ int attn_trace(unsigned long long* host, int n);   // trace build (tools/trace_a
 int last_trace(unsigned long long* host, int n);   // trace build (tools/trace_last.py)
 int token_x3_trace(unsigned long long* host, int n);   // trace build (tools/trace_token.py)
 int embed_trace(unsigned long long* host, int n);      // trace build (tools/trace_embed.py)
+int token_tc_trace(unsigned long long* host, int n);   // trace build (tools/trace_token.py fast)
 #endif
 cudaError_t launch_lossmask(const nvrec_lossmask_job* jobs, int n_jobs, cudaStream_t s);
 cudaError_t launch_baseline(int depth, int b, int h, int w, int c, const uint8_t* planes,

@@ -279,6 +279,35 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+// gelu_as (tile_ops.cuh) on a pair with packed fp32x2 FMA-pipe arithmetic:
+// the same operations in the same order per lane (bit-identical results),
+// about half the issue slots.
+__device__ __forceinline__ float2 gelu_as2(float2 v) {
+  const float2 k1 = make_float2(0.3275911f * 0.70710678118654752440f,
+                                0.3275911f * 0.70710678118654752440f);
+  const float2 one = make_float2(1.f, 1.f);
+  const float2 arg = ffma2(make_float2(fabsf(v.x), fabsf(v.y)), k1, one);
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(arg.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(arg.y));
+  float2 p = ffma2(t, make_float2(0.5f * 1.061405429f, 0.5f * 1.061405429f),
+                   make_float2(0.5f * -1.453152027f, 0.5f * -1.453152027f));
+  p = ffma2(p, t, make_float2(0.5f * 1.421413741f, 0.5f * 1.421413741f));
+  p = ffma2(p, t, make_float2(0.5f * -0.284496736f, 0.5f * -0.284496736f));
+  p = ffma2(p, t, make_float2(0.5f * 0.254829592f, 0.5f * 0.254829592f));
+  const float2 zero = make_float2(0.f, 0.f);
+  p = ffma2(p, t, zero);                                   // p * t
+  const float2 vv = ffma2(v, v, zero);
+  const float2 a = ffma2(vv, make_float2(-0.5f * 1.4426950408889634f, -0.5f * 1.4426950408889634f),
+                         zero);
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a.y));
+  const float2 h = ffma2(p, e, zero);                     // (1 - erf(|v|/sqrt 2)) / 2
+  const float2 omh = fadd2(one, make_float2(-h.x, -h.y));
+  return ffma2(v, make_float2(v.x >= 0.f ? omh.x : h.x, v.y >= 0.f ? omh.y : h.y), zero);
+}
+
 // 2^v for a pair v <= 0 on the FMA pipe (FA4-style MUFU offload): round to
 // the nearest integer j with the 1.5*2^23 trick, degree-3 polynomial for
 // 2^(v-j) on [-0.5, 0.5] (rel. error 6e-4, below bf16 P's 3.9e-3), then add
