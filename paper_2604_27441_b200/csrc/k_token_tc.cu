@@ -278,18 +278,32 @@ token_tc_kernel(TokenTcArgs a) {
     gemm_a(0, kOffFc1, 256);
     TT(8);
 #pragma unroll 1
-    for (int c8 = 0; c8 < 8; ++c8) {               // 8 chunks of 32 hidden units
-      uint32_t r[32], pk[16];
-      tmem_ld32(tbase + lane_off + 32 * c8, r);
-      tmem_wait_ld();
+    // 8 chunks of 32 hidden units; the TMEM load of chunk c+1 is in flight
+    // while chunk c is computed and stored (stores go to [16c, 16c+16), below
+    // every chunk still to be loaded)
+    {
+      uint32_t ra[32], rb[32];
+      auto gelu_store = [&](const uint32_t* r, int c8) {
+        uint32_t pk[16];
 #pragma unroll
-      for (int e = 0; e < 32; e += 2)
-      {
-        const float2 g = gelu_as2(make_float2(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e],
-                                              __uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
-        pk[e / 2] = pack_h2(g.x, g.y);
+        for (int e = 0; e < 32; e += 2) {
+          const float2 g = gelu_as2(make_float2(__uint_as_float(r[e]) + P_[kPBFc1 + 32 * c8 + e],
+                                                __uint_as_float(r[e + 1]) + P_[kPBFc1 + 32 * c8 + e + 1]));
+          pk[e / 2] = pack_h2(g.x, g.y);
+        }
+        tmem_st16(tbase + lane_off + 16 * c8, pk);   // columns [16 c8, 16 c8 + 16)
+      };
+      tmem_ld32(tbase + lane_off, ra);
+      tmem_wait_ld32(ra);
+#pragma unroll 1
+      for (int c8 = 0; c8 < 8; c8 += 2) {
+        tmem_ld32(tbase + lane_off + 32 * (c8 + 1), rb);
+        gelu_store(ra, c8);
+        tmem_wait_ld32(rb);
+        if (c8 + 2 < 8) tmem_ld32(tbase + lane_off + 32 * (c8 + 2), ra);
+        gelu_store(rb, c8 + 1);
+        if (c8 + 2 < 8) tmem_wait_ld32(ra);
       }
-      tmem_st16(tbase + lane_off + 16 * c8, pk);   // columns [16 c8, 16 c8 + 16)
     }
     tmem_wait_st();
     TT(9);
