@@ -748,8 +748,9 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         tma_load_3d(sm.v[s], &tm_v, &sm.kv_full[s], key0, 0, seq);
         tma_load_3d(sm.v[s] + kWVBytes / 2, &tm_v, &sm.kv_full[s], key0 + 64, 0, seq);
       }
-    } else if (warp == kMma && lane == 0) {
+    } else if (warp == kMma) {
       // ------------------------------------------------------------ MMA issuer
+      // (the whole warp runs the loop; one elected lane issues: *_w)
       const uint32_t qbase = smem_u32(sm.q[0]);
       constexpr uint32_t idS = idesc_bf16(128, kWTK);
       mbar_wait(&sm.q_full, 0);
@@ -768,9 +769,9 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
 #pragma unroll
           for (int u = 0; u < 6; ++u)
-            mma_ss(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
+            mma_ss_w(sc, sdesc(qb + qa[u] * 32, 1024, kSwizzle128B),
                    sdesc(kb + kc[u] * 32, 1024, kSwizzle128B), idS, u);
-          mma_commit(&sm.s_full[n % 3]);
+          mma_commit_w(&sm.s_full[n % 3]);
         }
         NVREC_TR(2, n, 1);
         const int m = n - 2;
@@ -788,11 +789,11 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
             const uint32_t vh = vb + (kk >> 2) * (kWVBytes / 2) + (kk & 3) * 32;
-            mma_ts(oc, ah, sdesc(vh, 1024, kSwizzle128B), kIdescPV64, kk);
-            mma_ts(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
+            mma_ts_w(oc, ah, sdesc(vh, 1024, kSwizzle128B), kIdescPV64, kk);
+            mma_ts_w(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
           }
-          mma_commit(&sm.pv_full[t]);
-          if (t == ntq - 1) mma_commit(&sm.kv_empty[s]);     // K/V(j) fully consumed
+          mma_commit_w(&sm.pv_full[t]);
+          if (t == ntq - 1) mma_commit_w(&sm.kv_empty[s]);     // K/V(j) fully consumed
         }
         NVREC_TR(2, n, 3);
       }

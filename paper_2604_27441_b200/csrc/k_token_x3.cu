@@ -12,7 +12,10 @@
 //   phase 1   x += fc2(GELU(fc1(LN_m(x))))                             128 KB
 //   phase 2   q,k,v = qkv_s'(LN_s'(x)) -> split bf16 attention operands  48 KB
 // Tiles, slots and the per-warp position layout follow k_token_tc.cu (lane =
-// j*nt + slice, the temporal attention is warp shuffles).  fc1 -> fc2 runs in
+// j*nt + slice, the temporal attention is warp shuffles); every row is held
+// by two threads (warps w and w + 4 of its slot, 32 columns each: one head of
+// the temporal attention and of q/k/v), which doubles the warps that hide the
+// TMEM / L2 latencies of this per-row work.  fc1 -> fc2 runs in
 // two halves of 128 hidden units: fc1 half -> TMEM, GELU written back in place
 // as fp16 [hi 32 | lo 32] column groups, fc2 reads them as the A operand from
 // TMEM; the accumulator sits beside the half (192 of the slot's 256 columns).
@@ -27,7 +30,10 @@ using namespace sm100;
 using namespace x3;
 
 constexpr int kSlots = 2;
-constexpr int kThreads = 128 * kSlots;
+// two threads per row: warps 8 slot + 4 hf + wq, hf = the row's column half
+// (32 of the 64 columns; one head of the temporal attention / of q, k, v)
+constexpr int kSlotThreads = 256;
+constexpr int kThreads = kSlotThreads * kSlots;
 // element offsets of the [hi | lo] packs inside one block's blk3 pack
 constexpr uint32_t kX3ProjS = 0, kX3QkvT = 8192, kX3ProjT = 32768, kX3Fc1 = 40960,
                    kX3Fc2 = 73728, kX3QkvS = 106496, kX3Blk = 131072;
@@ -47,6 +53,7 @@ struct __align__(128) X3Smem {
   __half w[ph_elems(PH)];
   uint8_t a[kSlots][2 * kABytes];   // per slot: A_hi | A_lo
   float par[kParFloats];
+  float2 red[kSlots][2][128];       // LayerNorm (mean, M2) of each row half
   uint64_t bar_w, bar_d[kSlots];
   uint32_t tmem_base;
 };
@@ -70,7 +77,7 @@ token_x3_kernel(TokenX3Args a) {
   using S = X3Smem<PH>;
   S& sm = *reinterpret_cast<S*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = warp >> 2, wq = warp & 3;        // tile slot, TMEM lane quarter
+  const int slot = warp >> 3, hf = (warp >> 2) & 1, wq = warp & 3;   // tile slot, half, lane quarter
   const int nt = a.nt;
   const int ppw = 32 / nt;                          // whole positions per warp
   const int P = 4 * ppw;                            // positions per tile
@@ -105,6 +112,7 @@ token_x3_kernel(TokenX3Args a) {
 
   const float* P_ = sm.par;
   const int m = wq * 32 + lane;                     // row == TMEM lane
+  const int c0 = 32 * hf;                           // this thread's first column
   const uint32_t lane_off = uint32_t(wq * 32) << 16;
   const uint32_t tbase = sm.tmem_base + 256 * slot; // this slot's 256 columns
   const int jl = lane / nt, it = lane - jl * nt;    // position in warp, slice
@@ -112,12 +120,13 @@ token_x3_kernel(TokenX3Args a) {
   uint8_t* A = sm.a[slot];
   const uint32_t ab = smem_u32(A);
   const uint32_t wb = smem_u32(sm.w) - ph_base(PH) * 2;   // + element offset * 2 = a block pack matrix
-  const bool issuer = wq == 0 && lane == 0;
+  const bool issuer = wq == 0 && hf == 0 && lane == 0;
+  auto slot_sync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(kSlotThreads) : "memory"); };
   uint32_t pd = 0;
   auto run = [&](auto issue) {
     fence_proxy_async();
     tc_fence_before();
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+    slot_sync();
     if (issuer) {
       tc_fence_after();
       issue();
@@ -145,14 +154,43 @@ token_x3_kernel(TokenX3Args a) {
   auto gemm_a = [&](uint32_t dcol, uint32_t woff, int N) {
     run([&] { issue_a(dcol, woff, N, N, 0); });
   };
-  // x += D[64 cols at col] * sc + bias
-  auto add64 = [&](float* x, uint32_t col, float sc, const float* bias) {
-    uint32_t r[64];
-    tmem_ld32(tbase + lane_off + col, r);
-    tmem_ld32(tbase + lane_off + col + 32, r + 32);
+  // x (this half) += D[32 cols at col + c0] * sc + bias
+  auto add32 = [&](float* x, uint32_t col, float sc, const float* bias) {
+    uint32_t r[32];
+    tmem_ld32(tbase + lane_off + col + c0, r);
     tmem_wait_ld();
 #pragma unroll
-    for (int e = 0; e < 64; ++e) x[e] += fmaf(__uint_as_float(r[e]), sc, bias[e]);
+    for (int e = 0; e < 32; ++e) x[e] += fmaf(__uint_as_float(r[e]), sc, bias[c0 + e]);
+  };
+  // LayerNorm of the row's 64 values held as two halves by two threads: local
+  // two-pass mean and M2 per half, one exchange, merged (Chan et al.) the same
+  // way in both threads; the normalised half goes straight into the A operand
+  float2* red = &sm.red[slot][0][0];
+  auto ln_put = [&](const float* x, const float* g, const float* bt) {
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int e = 0; e < 32; ++e) s4[e & 3] += x[e];
+    const float mh = ((s4[0] + s4[1]) + (s4[2] + s4[3])) * (1.f / 32.f);
+    float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int e = 0; e < 32; ++e) q4[e & 3] = fmaf(x[e] - mh, x[e] - mh, q4[e & 3]);
+    const float m2 = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+    red[hf * 128 + m] = make_float2(mh, m2);
+    slot_sync();
+    const float2 o = red[(hf ^ 1) * 128 + m];
+    const float d = mh - o.x;
+    const float mean = 0.5f * (mh + o.x);
+    const float rstd = rsqrtf((m2 + o.y + 16.f * d * d) * (1.f / 64.f) + 1e-5f);
+#pragma unroll
+    for (int ki = 0; ki < 4; ++ki) {
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = 8 * ki + j;
+        y[j] = (x[e] - mean) * rstd * g[c0 + e] + bt[c0 + e];
+      }
+      put_row_x3(A, m, y, 4 * hf + ki, 1);
+    }
   };
   const float scale = rsqrtf(32.f);
 
@@ -162,12 +200,12 @@ token_x3_kernel(TokenX3Args a) {
     const int b = tile / tiles_per_b;
     const int s = (tile - b * tiles_per_b) * P + wq * ppw + jl;
     const bool valid = row_live && s < a.ns;
-    const size_t xrow = (size_t(b * nt + it) * a.ns + s) * 64;
-    float x[64], y[64];
+    const size_t xrow = (size_t(b * nt + it) * a.ns + s) * 64 + c0;
+    float x[32];
     {
       const float4* xi = reinterpret_cast<const float4*>(a.x + xrow);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < 8; ++q) {
         float4 u = valid ? xi[q] : make_float4(0.f, 0.f, 0.f, 0.f);
         x[4 * q] = u.x; x[4 * q + 1] = u.y; x[4 * q + 2] = u.z; x[4 * q + 3] = u.w;
       }
@@ -175,88 +213,99 @@ token_x3_kernel(TokenX3Args a) {
     if constexpr (PH == 0) {
       // ---- x += proj_s(ao) ---------------------------------------------------
       {
+        float y[32];
         const float4* ai = reinterpret_cast<const float4*>(a.ao + xrow);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < 8; ++q) {
           float4 u = valid ? ai[q] : make_float4(0.f, 0.f, 0.f, 0.f);
           y[4 * q] = u.x; y[4 * q + 1] = u.y; y[4 * q + 2] = u.z; y[4 * q + 3] = u.w;
         }
+        TX(1);
+        put_row_x3(A, m, y, 4 * hf, 4);
       }
-      TX(1);
-      put_row_x3(A, m, y);
       gemm_a(0, kX3ProjS, 64);
       TX(2);
-      add64(x, 0, a.sc[0], P_ + kPBProjS);
-      // ---- qkv_t(LN_t(x)); temporal attention by warp shuffles ----------------
-      layernorm64(x, y, P_ + kPLnTw, P_ + kPLnTb);
-      put_row_x3(A, m, y);
+      add32(x, 0, a.sc[0], P_ + kPBProjS);
+      // ---- qkv_t(LN_t(x)); temporal attention (head hf) by warp shuffles -------
+      ln_put(x, P_ + kPLnTw, P_ + kPLnTb);
       TX(3);
       gemm_a(0, kX3QkvT, 192);
       TX(4);
       const float sq = a.sc[1];
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        float q[32], kk_[32], vv[32];
-        tmem_ld32(tbase + lane_off + 32 * hh, reinterpret_cast<uint32_t*>(q));
-        tmem_ld32(tbase + lane_off + 64 + 32 * hh, reinterpret_cast<uint32_t*>(kk_));
-        tmem_ld32(tbase + lane_off + 128 + 32 * hh, reinterpret_cast<uint32_t*>(vv));
+      const int l0 = jl * nt;                          // lane of slice 0
+      float sc[8];
+#pragma unroll
+      for (int ik = 0; ik < 8; ++ik) sc[ik] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {                    // 16 of the head's 32 dims at a time
+        float q[16], kk_[16];
+        tmem_ld16(tbase + lane_off + c0 + 16 * c, reinterpret_cast<uint32_t*>(q));
+        tmem_ld16(tbase + lane_off + 64 + c0 + 16 * c, reinterpret_cast<uint32_t*>(kk_));
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          q[e] = fmaf(q[e], sq, P_[kPBQkvT + 32 * hh + e]);
-          kk_[e] = fmaf(kk_[e], sq, P_[kPBQkvT + 64 + 32 * hh + e]);
-          vv[e] = fmaf(vv[e], sq, P_[kPBQkvT + 128 + 32 * hh + e]);
+        for (int e = 0; e < 16; ++e) {
+          q[e] = fmaf(q[e], sq, P_[kPBQkvT + c0 + 16 * c + e]);
+          kk_[e] = fmaf(kk_[e], sq, P_[kPBQkvT + 64 + c0 + 16 * c + e]);
         }
-        float sc[8];
-        float mx = -INFINITY;
-        const int l0 = jl * nt;                        // lane of slice 0
 #pragma unroll
         for (int ik = 0; ik < 8; ++ik) {
           if (ik >= nt) break;
-          float acc = 0.f;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) acc = fmaf(q[e], __shfl_sync(0xffffffffu, kk_[e], l0 + ik), acc);
-          sc[ik] = acc * scale;
-          mx = fmaxf(mx, sc[ik]);
+          for (int e = 0; e < 16; ++e) sc[ik] = fmaf(q[e], __shfl_sync(0xffffffffu, kk_[e], l0 + ik), sc[ik]);
         }
-        float den = 0.f;
+      }
+      float mx = -INFINITY;
 #pragma unroll
-        for (int ik = 0; ik < 8; ++ik) {
-          if (ik >= nt) break;
-          sc[ik] = expf(sc[ik] - mx);
-          den += sc[ik];
+      for (int ik = 0; ik < 8; ++ik) {
+        if (ik >= nt) break;
+        sc[ik] *= scale;
+        mx = fmaxf(mx, sc[ik]);
+      }
+      float den = 0.f;
+#pragma unroll
+      for (int ik = 0; ik < 8; ++ik) {
+        if (ik >= nt) break;
+        sc[ik] = expf(sc[ik] - mx);
+        den += sc[ik];
+      }
+      const float inv = 1.f / den;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float vv[16], o[16];
+        tmem_ld16(tbase + lane_off + 128 + c0 + 16 * c, reinterpret_cast<uint32_t*>(vv));
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          vv[e] = fmaf(vv[e], sq, P_[kPBQkvT + 128 + c0 + 16 * c + e]);
+          o[e] = 0.f;
         }
-        const float inv = 1.f / den;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) q[e] = 0.f;        // q -> output accumulator
 #pragma unroll
         for (int ik = 0; ik < 8; ++ik) {
           if (ik >= nt) break;
           const float p = sc[ik] * inv;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) q[e] = fmaf(p, __shfl_sync(0xffffffffu, vv[e], l0 + ik), q[e]);
+          for (int e = 0; e < 16; ++e) o[e] = fmaf(p, __shfl_sync(0xffffffffu, vv[e], l0 + ik), o[e]);
         }
         if (!row_live) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) q[e] = 0.f;
+          for (int e = 0; e < 16; ++e) o[e] = 0.f;
         }
-        put_row_x3(A, m, q, 4 * hh, 4);                // head hh -> A columns [32hh, 32hh+32)
+        put_row_x3(A, m, o, 4 * hf + 2 * c, 2);        // head hf -> A columns [32hf, 32hf+32)
       }
       // ---- x += proj_t(o) ------------------------------------------------------
       TX(5);
       gemm_a(0, kX3ProjT, 64);
       TX(6);
-      add64(x, 0, a.sc[2], P_ + kPBProjT);
+      add32(x, 0, a.sc[2], P_ + kPBProjT);
       if (valid) {
         float4* xo = reinterpret_cast<float4*>(a.x + xrow);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        for (int q = 0; q < 8; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
       }
     } else if constexpr (PH == 1) {
       // ---- x += fc2(GELU(fc1(LN_m(x)))) in two halves of 128 hidden units ------
       TX(1);
-      layernorm64(x, y, P_ + kPLnMw, P_ + kPLnMb);
-      put_row_x3(A, m, y);
+      ln_put(x, P_ + kPLnMw, P_ + kPLnMb);
       TX(2);
       const float s1 = a.sc[3], s2 = a.sc[4];
       // fc2 K step kk (16 hidden units of half H) from the TMEM column groups
@@ -273,46 +322,54 @@ token_x3_kernel(TokenX3Args a) {
           mma_ts(tbase + 128, ah + 32, wh, idesc, 1);
         }
       };
-      // GELU of the fc1 half in TMEM cols [0,128) -> [hi 32 | lo 32] per 64
+      // GELU of the fc1 half in TMEM cols [0,128) -> [hi 32 | lo 32] per 64;
+      // this thread's group is g = hf (cols 64 hf ..)
 #pragma unroll 1
       for (int H = 0; H < 2; ++H) {
         if (H == 0) run([&] { issue_a(0, kX3Fc1, 128, 256, 0); });
         else run([&] { issue_fc2(0); issue_a(0, kX3Fc1, 128, 256, 128); });
         TX(3 + 2 * H);
-#pragma unroll 1
-        for (int g = 0; g < 2; ++g) {
-          uint32_t r[64], lo[32];
-          tmem_ld32(tbase + lane_off + 64 * g, r);
-          tmem_ld32(tbase + lane_off + 64 * g + 32, r + 32);
-          tmem_wait_ld();
-          const float* bias = P_ + kPBFc1 + 128 * H + 64 * g;
+        const uint32_t gcol = tbase + lane_off + 64 * hf;
+        const float* bias = P_ + kPBFc1 + 128 * H + 64 * hf;
+        // values 0-31 -> hi pairs at cols 0-15 (stored at once), lo pairs at
+        // cols 32-47 (stored once values 32-63 have been read)
+        uint32_t r0[32], lo0[16];
+        tmem_ld32(gcol, r0);
+        tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 64; e += 2) {
-            const float2 g = gelu_as2(make_float2(fmaf(__uint_as_float(r[e]), s1, bias[e]),
-                                                  fmaf(__uint_as_float(r[e + 1]), s1, bias[e + 1])));
-            split_h2(g.x, g.y, r[e / 2], lo[e / 2]);
-          }
-          tmem_st16(tbase + lane_off + 64 * g, r);
-          tmem_st16(tbase + lane_off + 64 * g + 16, r + 16);
-          tmem_st16(tbase + lane_off + 64 * g + 32, lo);
-          tmem_st16(tbase + lane_off + 64 * g + 48, lo + 16);
+        for (int e = 0; e < 32; e += 2) {
+          const float2 g = gelu_as2(make_float2(fmaf(__uint_as_float(r0[e]), s1, bias[e]),
+                                                fmaf(__uint_as_float(r0[e + 1]), s1, bias[e + 1])));
+          split_h2(g.x, g.y, r0[e / 2], lo0[e / 2]);
         }
+        tmem_st16(gcol, r0);
+        uint32_t r1[32], lo1[16];
+        tmem_ld32(gcol + 32, r1);
+        tmem_wait_ld();
+        tmem_st16(gcol + 32, lo0);
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 g = gelu_as2(make_float2(fmaf(__uint_as_float(r1[e]), s1, bias[32 + e]),
+                                                fmaf(__uint_as_float(r1[e + 1]), s1, bias[33 + e])));
+          split_h2(g.x, g.y, r1[e / 2], lo1[e / 2]);
+        }
+        tmem_st16(gcol + 16, r1);
+        tmem_st16(gcol + 48, lo1);
         tmem_wait_st();
         TX(4 + 2 * H);
       }
       run([&] { issue_fc2(1); });
       TX(7);
-      add64(x, 128, s2, P_ + kPBFc2);
+      add32(x, 128, s2, P_ + kPBFc2);
       if (valid) {
         float4* xo = reinterpret_cast<float4*>(a.x + xrow);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        for (int q = 0; q < 8; ++q) xo[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
       }
     } else {
       // ---- next block's LN_s + qkv_s -> split bf16 attention operands ----------
       TX(1);
-      layernorm64(x, y, P_ + kPLnSw, P_ + kPLnSb);
-      put_row_x3(A, m, y);
+      ln_put(x, P_ + kPLnSw, P_ + kPLnSb);
       TX(2);
       gemm_a(0, kX3QkvS, 192);
       TX(3);
@@ -321,14 +378,15 @@ token_x3_kernel(TokenX3Args a) {
       const float sq = a.sc[5];
       __nv_bfloat16* vt = reinterpret_cast<__nv_bfloat16*>(A);
       const int jpos = wq * ppw + jl;                 // position inside the tile
+      const int head = hf;
+      const size_t seq = size_t(b * nt + it) * 2 + head;
 #pragma unroll 1
-      for (int c6 = 0; c6 < 6; ++c6) {
+      for (int which = 0; which < 3; ++which) {       // q, k, v of head hf: 32 columns
+        const int c6 = 2 * which + head;
         uint32_t r[32];
         tmem_ld32(tbase + lane_off + 32 * c6, r);
         tmem_wait_ld();
         if (!valid) continue;
-        const int which = c6 >> 1, head = c6 & 1;
-        const size_t seq = size_t(b * nt + it) * 2 + head;
         float v[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(r[e]), sq, P_[kPBQkvN + 32 * c6 + e]);
@@ -357,19 +415,20 @@ token_x3_kernel(TokenX3Args a) {
         }
       }
       // coalesced V^T stores: 8 consecutive positions (16 bytes) per store
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+      slot_sync();
       {
         const int s0 = (tile - b * tiles_per_b) * P;
         const int nvalid = min(P, a.ns - s0);
         const int cpr = (P + 7) / 8;                     // chunks per staged row
         const int rows = nt * 2 * 64;
-        // thread m owns chunk m % cpr of rows m / cpr, + 128 / cpr, ... (no
-        // division inside the loop)
-        const int rstep = 128 / cpr, ch = m % cpr, row0 = m / cpr;
+        // thread u of the slot owns chunk u % cpr of rows u / cpr, + 256 / cpr,
+        // ... (no division inside the loop)
+        const int u = hf * 128 + m;
+        const int rstep = kSlotThreads / cpr, ch = u % cpr, row0 = u / cpr;
         for (int row = row0; row0 < rstep && row < rows; row += rstep) {
           const int sl = row >> 6, e = row & 63;
-          const size_t seq = size_t(b * nt + (sl >> 1)) * 2 + (sl & 1);
-          __nv_bfloat16* dst = a.vth + (seq * 64 + e) * a.ns_pad + s0 + 8 * ch;
+          const size_t sq2 = size_t(b * nt + (sl >> 1)) * 2 + (sl & 1);
+          __nv_bfloat16* dst = a.vth + (sq2 * 64 + e) * a.ns_pad + s0 + 8 * ch;
           const __nv_bfloat16* src = vt + row * P + 8 * ch;
           if ((P & 7) == 0 && 8 * ch + 8 <= nvalid) {
             *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
@@ -379,7 +438,7 @@ token_x3_kernel(TokenX3Args a) {
         }
       }
       // the staging buffer is the next tile's A operand
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + slot) : "memory");
+      slot_sync();
     }
     // every thread's TMEM reads precede the next tile's first MMA (run()'s barrier)
     TX(15);

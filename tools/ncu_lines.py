@@ -31,6 +31,8 @@ def main(rep, obj, top=25, kre=None, fsub=None):
     rows = list(csv.reader(io.StringIO(out)))
     hdr, data = rows[1], rows[2:]
     ai = hdr.index("Warp Stall Sampling (All Samples)")
+    # per-reason columns (stall_*, all samples)
+    rcols = [(i, h[6:]) for i, h in enumerate(hdr) if h.startswith("stall_") and "(" not in h]
     # the kernel's own function in the cubin: match by instruction count order
     kname = rows[0][1].split("(")[0].split("::")[-1]
     funcs, cur, cur_fn = {}, None, None
@@ -46,7 +48,8 @@ def main(rep, obj, top=25, kre=None, fsub=None):
         m2 = re.match(r'\s+/\*([0-9a-f]{4,})\*/', line)
         if m2 and cur and cur_fn:
             funcs[cur_fn][int(m2.group(1), 16)] = cur
-    cands = [f for f in funcs if kname in f and (not fsub or fsub in f)] or list(funcs)
+    kname = kname.split("<")[0]
+    cands = [f for f in funcs if (fsub in f if fsub else kname in f)] or list(funcs)
     base = int(data[0][0], 16)
     def fl(x):
         try:
@@ -55,7 +58,7 @@ def main(rep, obj, top=25, kre=None, fsub=None):
             return 0.0
     tot = sum(fl(r[ai]) for r in data if len(r) > ai) or 1.0
     for fn in cands:
-        agg = {}
+        agg, why = {}, {}
         for r in data:
             if len(r) <= ai:
                 continue
@@ -64,9 +67,17 @@ def main(rep, obj, top=25, kre=None, fsub=None):
             except ValueError:
                 continue
             agg[key] = agg.get(key, 0.0) + fl(r[ai])
+            w = why.setdefault(key, {})
+            for i, nm in rcols:
+                if i < len(r):
+                    w[nm] = w.get(nm, 0.0) + fl(r[i])
         print("==", fn)
         for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
-            print("%5.1f%% %s:%d" % (100 * v / tot, k[0], k[1]))
+            w = why.get(k, {})
+            tw = sum(w.values()) or 1.0
+            rs = ", ".join("%s %d%%" % (n, 100 * c / tw) for n, c in
+                           sorted(w.items(), key=lambda x: -x[1])[:3] if c > 0)
+            print("%5.1f%% %-26s %s" % (100 * v / tot, "%s:%d" % k, rs))
 
 
 if __name__ == "__main__":

@@ -243,13 +243,20 @@ void run(const char* name, int warps, double bytes_per_cta) {
 // addresses: Q of 2 query tiles (16 KB each), K/V in a 4-stage ring (16 KB +
 // 16 KB per key tile, key tile j = n / 2), S buffers n % 3, O' per tile.  rot = 0
 // reuses stage 0 every time (operands possibly cached), rot = 1 rotates.
-__global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int rot, int qtmem) {
+__global__ void __launch_bounds__(512, 1) rot_bench(unsigned long long* cyc, int rot, int qtmem, int rnd, int fix) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   __shared__ uint32_t tbase;
   __shared__ uint64_t bar;
   uint8_t* base = dsm + ((1024 - (smem_u32(dsm) & 1023)) & 1023);
-  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+  // operands: zeros, or (rnd) bf16 values in [-2, 2) from a hash, so that the
+  // tensor datapath toggles as it does on real data
+  const int nw = (fix & 16) ? 40 * 1024 / 4 : 160 * 1024 / 4;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+    uint32_t h = (uint32_t(i) + 0x9e3779b9u * (blockIdx.x + 1)) * 0x85ebca6bu;
+    h ^= h >> 13; h *= 0xc2b2ae35u; h ^= h >> 16;
+    const uint32_t v = rnd ? ((0x3f80u | (h & 0x807fu)) | ((0x3f80u | ((h >> 16) & 0x807fu)) << 16)) : 0u;
+    reinterpret_cast<uint32_t*>(base)[i] = v;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -260,6 +267,22 @@ __global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int
   __syncthreads();
   tc_fence_after();
   const uint32_t t = tbase;
+  if (rnd) {   // P/S columns: the same kind of bf16 pairs (each warp its lane quarter)
+    const uint32_t lo = uint32_t((threadIdx.x >> 5) * 32) << 16;
+    for (int c = 0; c < 512; c += 32) {
+      uint32_t r[32];
+      for (int e = 0; e < 32; ++e) {
+        uint32_t h = (uint32_t(threadIdx.x * 512 + c + e) + 0x7f4a7c15u * (blockIdx.x + 1)) * 0x85ebca6bu;
+        h ^= h >> 15;
+        r[e] = (0x3f00u | (h & 0x807fu)) | ((0x3f00u | ((h >> 16) & 0x807fu)) << 16);
+      }
+      tmem_st32(t + lo + c, r);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   unsigned long long t0 = clock64();
   if (threadIdx.x == 0) {
     const uint32_t q0 = smem_u32(base), k0 = q0 + 32768, v0 = k0 + 4 * 16384;
@@ -267,9 +290,10 @@ __global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int
                        idP32 = idesc_bf16(128, 32);
     constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kc[6] = {0, 1, 2, 3, 0, 1};
     for (int n = 0; n < 2048; ++n) {
-      const int tq = n & 1, j = n >> 1, st = rot ? (j & 3) : 0;
+      const int tq = (fix & 1) ? 0 : (n & 1), j = n >> 1, st = rot ? (j & 3) : 0;
       const uint32_t sc = t + (n % 3) * 128;
-      const uint32_t qb = q0 + tq * 16384, kb = k0 + st * 16384;
+      uint32_t qb = q0 + tq * 16384, kb = k0 + st * 16384;
+      if (fix & 4) { qb = q0; kb = q0 + 8192; }        // mode 6's overlapping operands
 #pragma unroll
       for (int u = 0; u < 6; ++u) {
         if (qtmem)   // A (Q) from TMEM columns of the O' area (timing only)
@@ -280,8 +304,10 @@ __global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int
       }
       if (n >= 2) {
         const int m = n - 2, jm = m >> 1, sv = rot ? (jm & 3) : 0;
-        const uint32_t bc = t + (m % 3) * 128, oc = t + 384 + 64 * (m & 1);
-        const uint32_t vb = v0 + sv * 16384;
+        const uint32_t bc = t + (m % 3) * 128, oc = t + 384 + ((fix & 2) ? 0 : 64 * (m & 1));
+        uint32_t vb = v0 + sv * 16384;
+        if (fix & 4) vb = q0 + 24576;
+        if (fix & 8) vb = k0 + sv * 16384;              // V = the K stage (same lines)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
@@ -302,21 +328,23 @@ __global__ void __launch_bounds__(128, 1) rot_bench(unsigned long long* cyc, int
   if (threadIdx.x < 32) tmem_dealloc<512>(t);
 }
 
-void run_rot(int rot, int qtmem) {
+void run_rot(int rot, int qtmem, int rnd = 0, int fix = 0) {
   unsigned long long* cyc;
   cudaMalloc(&cyc, 148 * 8);
-  const int smem = 160 * 1024 + 1024;
-  cudaFuncSetAttribute(rot_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  rot_bench<<<148, 128, smem>>>(cyc, rot, qtmem);
+  // fix & 16 (with fix & 4: operands inside 40 KB): 41 KB of dynamic smem; fix & 32: 512 threads
+  const int smem = (fix & 16) ? 41 * 1024 : 160 * 1024 + 1024;
+  const int thr = (fix & 32) ? 512 : 128;
+  cudaFuncSetAttribute(rot_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024 + 1024);
+  rot_bench<<<148, thr, smem>>>(cyc, rot, qtmem, rnd, fix);
   cudaDeviceSynchronize();
-  rot_bench<<<148, 128, smem>>>(cyc, rot, qtmem);
+  rot_bench<<<148, thr, smem>>>(cyc, rot, qtmem, rnd, fix);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, cyc, sizeof h, cudaMemcpyDeviceToHost);
   double mean = 0;
   for (int i = 0; i < 148; ++i) mean += double(h[i]) / 148;
-  printf("x3w MMA stream, kernel operand layout, rotate=%d Q-in-TMEM=%d: %.1f clk/S tile (%s)\n",
-         rot, qtmem, mean / 2048.0, cudaGetErrorString(e));
+  printf("x3w MMA stream, kernel operand layout, rotate=%d Q-in-TMEM=%d operands=%s fixQ=%d fixO=%d fix=%d: %.1f clk/S tile (%s)\n",
+         rot, qtmem, rnd ? "random" : "zero", fix & 1, fix >> 1 & 1, fix, mean / 2048.0, cudaGetErrorString(e));
   cudaFree(cyc);
 }
 
@@ -324,6 +352,16 @@ int main() {
   run_rot(0, 0);
   run_rot(1, 0);
   run_rot(1, 1);
+  run_rot(1, 0, 1);
+  run_rot(1, 1, 1);
+  run_rot(0, 0, 1);
+  run_rot(0, 0, 0, 32);
+  run_rot(0, 0, 0, 16 + 4);
+  run_rot(0, 0, 0, 16 + 4 + 3);
+  run_rot(0, 0, 0, 16 + 32 + 4 + 3);
+  const double ab0 = double(kIters) * 8 * 4096;
+  run<6, 128, 1>("x3w MMA stream (S 6xN128 + PV 8x(N64+N32))", 1, ab0);
+  run<8, 128, 1>("x3w MMA stream + commits (mask)", 0, ab0);
   return 0;
   for (int w : {1, 2, 4, 8, 16}) {
     const double bytes = double(w) * kIters * 4 * 32 * 32 * 4;   // warps x iters x 4 x (32 lanes x 32 cols x 4 B)
