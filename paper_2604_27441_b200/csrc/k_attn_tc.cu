@@ -291,7 +291,23 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
     } else if (warp == kMma) {
       // ---------------------------------------------------------- MMA issuer
-      if (lane == 0) {
+      // x3 (split operands, 22 MMAs per key tile): the whole warp runs the
+      // loop and one elected lane issues (*_w: no per-MMA ELECT loop); the
+      // bf16 variant (3 MMAs per key tile, softmax-bound) measured faster
+      // with lane 0 alone
+      if (kX3 || lane == 0) {
+        auto mss = [&](uint32_t d, uint64_t a_, uint64_t b_, uint32_t id, uint32_t acc) {
+          if constexpr (kX3) mma_ss_w(d, a_, b_, id, acc);
+          else mma_ss(d, a_, b_, id, acc);
+        };
+        auto mts = [&](uint32_t d, uint32_t a_, uint64_t b_, uint32_t id, uint32_t acc) {
+          if constexpr (kX3) mma_ts_w(d, a_, b_, id, acc);
+          else mma_ts(d, a_, b_, id, acc);
+        };
+        auto mcommit = [&](uint64_t* bar) {
+          if constexpr (kX3) mma_commit_w(bar);
+          else mma_commit(bar);
+        };
         constexpr int QK = kX3 ? 4 : 2;            // K16 chunks per Q/K row
         uint64_t qdesc[kQT][QK];
         for (int t = 0; t < kQT; ++t)
@@ -314,16 +330,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                 constexpr int qa[6] = {0, 1, 0, 1, 2, 3}, kb_[6] = {0, 1, 2, 3, 0, 1};
 #pragma unroll
                 for (int u = 0; u < 6; ++u)
-                  mma_ss(sc, qdesc[t][qa[u]], sdesc(kb + kb_[u] * 32, G::Sbo, G::Sw), idS, u);
+                  mss(sc, qdesc[t][qa[u]], sdesc(kb + kb_[u] * 32, G::Sbo, G::Sw), idS, u);
               } else {
                 if (j >= 2) {
                   mbar_wait_fast(&sm.o_read[t], (go[t] + j - 2) & 1);
                   tc_fence_after();
                 }
                 for (int kk = 0; kk < 2; ++kk)
-                  mma_ss(sc, qdesc[t][kk], sdesc(kb + kk * 32, G::Sbo, G::Sw), idS, kk);
+                  mss(sc, qdesc[t][kk], sdesc(kb + kk * 32, G::Sbo, G::Sw), idS, kk);
               }
-              mma_commit(&sm.s_full[t][(gs[t] + j) & 1]);
+              mcommit(&sm.s_full[t][(gs[t] + j) & 1]);
             }
           }
           if (j >= 1) {
@@ -340,22 +356,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                   const uint32_t vh = vb + kk * 32;
-                  mma_ts(oc, bc + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, kk);
-                  mma_ts(oc, bc + kk * 8, sdesc(vh + 4096, 1024, kSwizzle128B), kIdescPV, 1);
-                  mma_ts(oc, bc + 32 + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
+                  mts(oc, bc + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, kk);
+                  mts(oc, bc + kk * 8, sdesc(vh + 4096, 1024, kSwizzle128B), kIdescPV, 1);
+                  mts(oc, bc + 32 + kk * 8, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
                 }
               } else {
                 for (int kk = 0; kk < 8; ++kk) {   // chunk kk/4 of V^T, 32 B apart
                   const uint32_t addr = vb + (kk >> 2) * (G::VBytes / 2) + (kk & 3) * 32;
-                  mma_ts(oc, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
+                  mts(oc, bc + kk * 8, sdesc(addr, 1024, kSwizzle128B), kIdescPV, kk);
                 }
               }
-              mma_commit(&sm.pv_full[t]);
+              mcommit(&sm.pv_full[t]);
             }
-            mma_commit(&sm.kv_empty[sp]);               // K/V_{j-1} fully consumed
+            mcommit(&sm.kv_empty[sp]);               // K/V_{j-1} fully consumed
           }
         }
-        mma_commit(&sm.done);             // the group's MMAs (Q reads) are complete
+        mcommit(&sm.done);             // the group's MMAs (Q reads) are complete
         mbar_wait(&sm.done, gq & 1);
       }
     }

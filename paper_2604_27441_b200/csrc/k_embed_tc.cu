@@ -243,7 +243,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA
-    if (lane == 0) {
+    {   // the whole warp runs the loop; one elected lane issues (*_w)
       const uint32_t idesc = idesc_f16(128, 64);
       for (int st = 0; st < nst; ++st) {
         const int ps = st % S::kNst, pw = st % S::kNw;
@@ -257,17 +257,17 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
 #pragma unroll
         for (int kk = 0; kk < S::kKst / 16; ++kk) {
           const uint64_t ad = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
-          mma_ss(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
+          mma_ss_w(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
           if (X3)   // pixels are exact: pix . W_lo completes the product
-            mma_ss(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+            mma_ss_w(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
           if (F32 && X3)   // float inputs: + x_lo . W_hi
-            mma_ss(tmem, sdesc(ab + S::kA1 + kk * 4096, 128, kSwizzleNone, 2048),
+            mma_ss_w(tmem, sdesc(ab + S::kA1 + kk * 4096, 128, kSwizzleNone, 2048),
                    sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
         }
-        mma_commit(&sm.empty[ps]);
-        mma_commit(&sm.w_empty[pw]);
+        mma_commit_w(&sm.empty[ps]);
+        mma_commit_w(&sm.w_empty[pw]);
       }
-      mma_commit(&sm.acc_full);
+      mma_commit_w(&sm.acc_full);
       mbar_wait(&sm.wq_full, 0);
       mbar_wait(&sm.a2_ready, 0);
       tc_fence_after();
@@ -277,15 +277,15 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t yh = sdesc(a2b + kk * 4096, 128, kSwizzleNone, 2048);
         const uint64_t wh = sdesc(wqb + kk * 6144, 128, kSwizzleNone, 3072);
-        mma_ss(tmem + 64, yh, wh, idesc2, kk != 0);
+        mma_ss_w(tmem + 64, yh, wh, idesc2, kk != 0);
         if (X3) {   // y_hi W_lo + y_lo W_hi
-          mma_ss(tmem + 64, yh, sdesc(wqb + S::kQkvW1 + kk * 6144, 128, kSwizzleNone, 3072),
+          mma_ss_w(tmem + 64, yh, sdesc(wqb + S::kQkvW1 + kk * 6144, 128, kSwizzleNone, 3072),
                  idesc2, 1);
-          mma_ss(tmem + 64, sdesc(a2b + S::kA21 + kk * 4096, 128, kSwizzleNone, 2048), wh,
+          mma_ss_w(tmem + 64, sdesc(a2b + S::kA21 + kk * 4096, 128, kSwizzleNone, 2048), wh,
                  idesc2, 1);
         }
       }
-      mma_commit(&sm.qkv_full);
+      mma_commit_w(&sm.qkv_full);
     }
   } else {
     // ------------------------------------------------- converters, then epilogue

@@ -215,11 +215,12 @@ last_tc_kernel(LastTcArgs a) {
     __syncthreads();
     tc_fence_after();
   };
+  const bool w0 = warp == 0;            // MMA issue: warp 0, one elected lane (*_w)
   auto run = [&](auto issue) {
     sync_mma();
-    if (t0) {
+    if (w0) {
       issue();
-      mma_commit(&sm.bar_d);
+      mma_commit_w(&sm.bar_d);
     }
     mbar_wait(&sm.bar_d, pd & 1);
     ++pd;
@@ -236,9 +237,9 @@ last_tc_kernel(LastTcArgs a) {
       const uint64_t al = sdesc(ab + kABytes + kk * 4096, 128, kSwizzleNone, 2048);
       const uint64_t wh = sdesc(bh + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
       const uint64_t wl = sdesc(bl + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
-      mma_ss(tbase + dcol, ah, wh, idesc, kk != 0);
-      mma_ss(tbase + dcol, ah, wl, idesc, 1);
-      mma_ss(tbase + dcol, al, wh, idesc, 1);
+      mma_ss_w(tbase + dcol, ah, wh, idesc, kk != 0);
+      mma_ss_w(tbase + dcol, ah, wl, idesc, 1);
+      mma_ss_w(tbase + dcol, al, wh, idesc, 1);
     }
   };
   // x[16] += D[16 cols at col] * sc + bias
@@ -375,9 +376,9 @@ last_tc_kernel(LastTcArgs a) {
           const uint64_t wh = sdesc(bh + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
           const uint64_t wl = sdesc(bl + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
           const uint32_t d = tbase + 192 + 128 * it;
-          mma_ss(d, ah, wh, idesc, kk != 0);
-          mma_ss(d, ah, wl, idesc, 1);
-          mma_ss(d, al, wh, idesc, 1);
+          mma_ss_w(d, ah, wh, idesc, kk != 0);
+          mma_ss_w(d, ah, wl, idesc, 1);
+          mma_ss_w(d, al, wh, idesc, 1);
         }
       }
     });
@@ -470,9 +471,9 @@ last_tc_kernel(LastTcArgs a) {
           const uint32_t ah = tbase + (kk >> 2) * 64 + (kk & 3) * 8;
           const uint64_t wh = sdesc(bh + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
           const uint64_t wl = sdesc(bl + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
-          mma_ts(tbase + 128, ah, wh, idesc, H != 0 || kk != 0);
-          mma_ts(tbase + 128, ah, wl, idesc, 1);
-          mma_ts(tbase + 128, ah + 32, wh, idesc, 1);
+          mma_ts_w(tbase + 128, ah, wh, idesc, H != 0 || kk != 0);
+          mma_ts_w(tbase + 128, ah, wl, idesc, 1);
+          mma_ts_w(tbase + 128, ah + 32, wh, idesc, 1);
         }
       };
 #pragma unroll 1
@@ -533,11 +534,11 @@ last_tc_kernel(LastTcArgs a) {
       const int ci = ci0 + kBlkChunks + i;
       wait_chunk(ci);
       issue_a(0, 256 * (i & 1), wsm(ci), nc);
-      mma_commit(&sm.bar_h[i & 1]);
+      mma_commit_w(&sm.bar_h[i & 1]);
     };
     LT(14);
     sync_mma();
-    if (t0) issue_head(0);
+    if (w0) issue_head(0);
     const int ih = s / a.nw, iw = s - (s / a.nw) * a.nw;
     uint8_t* ob = nullptr;
     const int pix_bytes = a.u16 ? 2 * c : c;                      // u16 depth: 2 bytes
@@ -551,7 +552,7 @@ last_tc_kernel(LastTcArgs a) {
         // every thread has read chunk i-1's columns, which chunk i+1 reuses
         tc_fence_before();
         __syncthreads();
-        if (t0) {
+        if (w0) {
           tc_fence_after();
           issue_head(i + 1);
         }

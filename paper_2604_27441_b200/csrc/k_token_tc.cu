@@ -128,9 +128,9 @@ token_tc_kernel(TokenTcArgs a) {
   const bool row_live = jl < ppw;
   uint8_t* A = sm.a[slot];
   const uint32_t ab = smem_u32(A), wb = smem_u32(sm.w);
-  const bool issuer = wq == 0 && lane == 0;
+  const bool issuer = wq == 0;                  // warp: one elected lane issues (*_w)
   uint32_t pd = 0;
-  // all 128 threads of the slot have written their operands -> one thread
+  // all 128 threads of the slot have written their operands -> one warp
   // issues the GEMM, everybody waits for the accumulator
   auto run = [&](auto issue) {
     fence_proxy_async();
@@ -139,7 +139,7 @@ token_tc_kernel(TokenTcArgs a) {
     if (issuer) {
       tc_fence_after();
       issue();
-      mma_commit(&sm.bar_d[slot]);
+      mma_commit_w(&sm.bar_d[slot]);
     }
     mbar_wait(&sm.bar_d[slot], pd & 1);
     ++pd;
@@ -150,7 +150,7 @@ token_tc_kernel(TokenTcArgs a) {
       const uint32_t idesc = idesc_f16(128, N), lbo_b = (N / 8) * 128;
       const uint32_t bbase = wb + woff * 2;
       for (int kk = 0; kk < 4; ++kk)
-        mma_ss(tbase + dcol, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
+        mma_ss_w(tbase + dcol, sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048),
                sdesc(bbase + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b), idesc, kk != 0);
     });
   };
@@ -312,7 +312,7 @@ token_tc_kernel(TokenTcArgs a) {
       const uint32_t idesc = idesc_f16(128, 64), lbo_b = 8 * 128;
       const uint32_t bbase = wb + kOffFc2 * 2;
       for (int kk = 0; kk < 16; ++kk)
-        mma_ts(tbase + 128, tbase + kk * 8, sdesc(bbase + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b),
+        mma_ts_w(tbase + 128, tbase + kk * 8, sdesc(bbase + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b),
                idesc, kk != 0);
     });
     TT(10);

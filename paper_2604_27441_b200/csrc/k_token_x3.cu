@@ -120,7 +120,7 @@ token_x3_kernel(TokenX3Args a) {
   uint8_t* A = sm.a[slot];
   const uint32_t ab = smem_u32(A);
   const uint32_t wb = smem_u32(sm.w) - ph_base(PH) * 2;   // + element offset * 2 = a block pack matrix
-  const bool issuer = wq == 0 && hf == 0 && lane == 0;
+  const bool issuer = wq == 0 && hf == 0;       // warp: one elected lane issues (*_w)
   auto slot_sync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(kSlotThreads) : "memory"); };
   uint32_t pd = 0;
   auto run = [&](auto issue) {
@@ -130,7 +130,7 @@ token_x3_kernel(TokenX3Args a) {
     if (issuer) {
       tc_fence_after();
       issue();
-      mma_commit(&sm.bar_d[slot]);
+      mma_commit_w(&sm.bar_d[slot]);
     }
     mbar_wait(&sm.bar_d[slot], pd & 1);
     ++pd;
@@ -146,9 +146,9 @@ token_x3_kernel(TokenX3Args a) {
       const uint64_t al = sdesc(ab + kABytes + kk * 4096, 128, kSwizzleNone, 2048);
       const uint64_t wh = sdesc(bh + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
       const uint64_t wl = sdesc(bl + kk * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
-      mma_ss(tbase + dcol, ah, wh, idesc, kk != 0);
-      mma_ss(tbase + dcol, ah, wl, idesc, 1);
-      mma_ss(tbase + dcol, al, wh, idesc, 1);
+      mma_ss_w(tbase + dcol, ah, wh, idesc, kk != 0);
+      mma_ss_w(tbase + dcol, ah, wl, idesc, 1);
+      mma_ss_w(tbase + dcol, al, wh, idesc, 1);
     }
   };
   auto gemm_a = [&](uint32_t dcol, uint32_t woff, int N) {
@@ -317,9 +317,9 @@ token_x3_kernel(TokenX3Args a) {
           const uint32_t ah = tbase + (kk >> 2) * 64 + (kk & 3) * 8;
           const uint64_t wh = sdesc(bh + kg * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
           const uint64_t wl = sdesc(bl + kg * 2 * lbo_b, 128, kSwizzleNone, lbo_b);
-          mma_ts(tbase + 128, ah, wh, idesc, kg != 0);
-          mma_ts(tbase + 128, ah, wl, idesc, 1);
-          mma_ts(tbase + 128, ah + 32, wh, idesc, 1);
+          mma_ts_w(tbase + 128, ah, wh, idesc, kg != 0);
+          mma_ts_w(tbase + 128, ah, wl, idesc, 1);
+          mma_ts_w(tbase + 128, ah + 32, wh, idesc, 1);
         }
       };
       // GELU of the fc1 half in TMEM cols [0,128) -> [hi 32 | lo 32] per 64;
