@@ -647,6 +647,24 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
         }
       return base;
     };
+    // [hi ; lo] stacked as ONE 2N-row B operand (N = 64 -> an N = 128 MMA
+    // computes A W_hi and A W_lo side by side; the epilogue adds the halves):
+    // the same core-matrix layout as pack2 with 2N rows
+    auto pack2m = [&](int N, int K, auto at, int sexp) {
+      const size_t base = h3.size();
+      h3.resize(base + 2 * size_t(N) * K);
+      for (int n = 0; n < N; ++n)
+        for (int k = 0; k < K; ++k) {
+          const float v = std::ldexp(at(n, k), sexp);
+          const __half hi = __float2half_rn(v);
+          for (int part = 0; part < 2; ++part) {
+            const int r = n + part * N;
+            const size_t idx = (size_t(k / 8) * (2 * N / 8) + r / 8) * 64 + (r % 8) * 8 + k % 8;
+            h3[base + idx] = part ? __float2half_rn(v - __half2float(hi)) : hi;
+          }
+        }
+      return base;
+    };
     auto maxabs = [](int N, int K, auto at) {
       float mx = 0.f;
       for (int n = 0; n < N; ++n)
@@ -666,7 +684,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
     size_t emb3_off = 0;
     for (int st = 0; st < T * 16 / kpy3; ++st) {
       const int tt = st / (16 / kpy3), py0 = kpy3 * (st % (16 / kpy3));
-      const size_t o = pack2(d, kst3, [&](int n, int k) {
+      const size_t o = pack2m(d, kst3, [&](int n, int k) {
         const int pyl = k / (16 * c), rem = k % (16 * c), px = rem / c, ci = rem % c;
         return ew_at(n, ci, tt, py0 + pyl, px);
       }, se);
@@ -696,7 +714,7 @@ int nvrec_model_load(nvrec_model* m, const float* const* t, const int64_t* numel
       const int s16 = exponent_for(256.f * emx);
       m->W.tc.sc_emb16 = std::ldexp(1.f, -s16);
       for (int st = 0; st < T * 16; ++st) {             // one patch row per X3 stage
-        const size_t o = pack2(d, 32, at16(st / 16, st % 16), s16);
+        const size_t o = pack2m(d, 32, at16(st / 16, st % 16), s16);
         if (st == 0) emb16_3_off = o;
       }
     }

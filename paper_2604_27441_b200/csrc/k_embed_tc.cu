@@ -12,7 +12,8 @@
 //   warps 0-3  converters: u8 -> fp16 (exact: byte_perm into 1024+v, then
 //              -1024) written as the UMMA A operand (no-swizzle K-major core
 //              matrices); masked patches of the corrupted frame become zeros
-//   warp 5     MMA: D[128 x 64] += A[128 x 32c] W^T per stage (fp32 in TMEM),
+//   warp 5     MMA: D[128 x 64] += A[128 x 32c] W^T per stage (fp32 in TMEM;
+//              the u8 / u16 split variants: D[128 x 128] = A [W_hi ; W_lo]^T),
 //              then the qkv GEMM [128 x 64] x [64 x 192] on the LN output
 //   warps 0-3  epilogue: TMEM -> registers (one token row per thread),
 //              x = acc/255 + bias + time_pos (+ sum of mask-channel weights),
@@ -157,6 +158,8 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   // F32: T x C x 8 image stages (2 rows of one channel of one sub-frame), then
   // 8 mask-channel stages on the last slice (model.py:105-107: the mask channel
   // is nonzero only in the stack's last frame)
+  // u8 / u16 split variants: [W_hi ; W_lo] stacked into one N = 128 operand
+  constexpr bool kStacked = X3 && !F32;
   const bool last_slice_cta = it == a.D.nt - 1;
   const int nimg = F32 ? T * C * 8 : T * S::kSpt;
   const int nst = nimg + (F32 && last_slice_cta ? 8 : 0);
@@ -244,7 +247,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA
     {   // the whole warp runs the loop; one elected lane issues (*_w)
-      const uint32_t idesc = idesc_f16(128, 64);
+      const uint32_t idesc = idesc_f16(128, 64), idesc128 = idesc_f16(128, 128);
       for (int st = 0; st < nst; ++st) {
         const int ps = st % S::kNst, pw = st % S::kNw;
         ET(st, 0);
@@ -257,12 +260,19 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
 #pragma unroll
         for (int kk = 0; kk < S::kKst / 16; ++kk) {
           const uint64_t ad = sdesc(ab + kk * 4096, 128, kSwizzleNone, 2048);
-          mma_ss_w(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
-          if (X3)   // pixels are exact: pix . W_lo completes the product
-            mma_ss_w(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
-          if (F32 && X3)   // float inputs: + x_lo . W_hi
-            mma_ss_w(tmem, sdesc(ab + S::kA1 + kk * 4096, 128, kSwizzleNone, 2048),
-                   sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+          if constexpr (kStacked) {
+            // pixels are exact: pix . [W_hi ; W_lo] as one N = 128 MMA (the
+            // stacked pack, LBO 2048); D[0,64) + D[64,128) in the epilogue
+            mma_ss_w(tmem, ad, sdesc(wb + kk * 4096, 128, kSwizzleNone, 2048), idesc128,
+                     (st | kk) != 0);
+          } else {
+            mma_ss_w(tmem, ad, sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, (st | kk) != 0);
+            if (F32 && X3)   // float inputs: + x_hi . W_lo + x_lo . W_hi
+              mma_ss_w(tmem, ad, sdesc(wb + S::kW1 + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+            if (F32 && X3)
+              mma_ss_w(tmem, sdesc(ab + S::kA1 + kk * 4096, 128, kSwizzleNone, 2048),
+                       sdesc(wb + kk * 2048, 128, kSwizzleNone, 1024), idesc, 1);
+          }
         }
         mma_commit_w(&sm.empty[ps]);
         mma_commit_w(&sm.w_empty[pw]);
@@ -400,6 +410,12 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[32 * h + j] = __uint_as_float(r[j]);
+        if constexpr (kStacked) {       // + pix . W_lo (columns 64..127)
+          tmem_ld32(tmem + lane_off + 64 + 32 * h, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) x[32 * h + j] += __uint_as_float(r[j]);
+        }
       }
     }
     const bool mterm = !F32 && last_slice && masked;   // F32: the mask channel is in the GEMM
@@ -459,6 +475,7 @@ embed_tc_kernel(const __grid_constant__ CUtensorMap tm_u8, EmbedTcArgs a, TcW tc
       }
     }
     fence_proxy_async();
+    tc_fence_before();     // the accumulator reads precede the qkv MMA (it reuses columns 64..127)
     mbar_arrive(&sm.a2_ready);
     EE(2);
     // ---- epilogue 2: q, k, v (+ bias) -> bf16 attention operands -----------
