@@ -805,7 +805,7 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t ah = bc + (kk >> 2) * 64 + (kk & 3) * 8;
             const uint32_t vh = vb + (kk >> 2) * (kWVBytes / 2) + (kk & 3) * 32;
-            mma_ts_w(oc, ah, sdesc(vh, 1024, kSwizzle128B), kIdescPV64, kk);
+            mma_ts_w(oc, ah, sdesc(vh, 1024, kSwizzle128B), kIdescPV64, (j | kk) != 0);
             mma_ts_w(oc, ah + 32, sdesc(vh, 1024, kSwizzle128B), kIdescPV, 1);
           }
           mma_commit_w(&sm.pv_full[t]);
@@ -820,29 +820,14 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     const int t = warp >> 2, quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    float m = -INFINITY, l = 0.f, a_prev = 0.f;
-    float2 o2[kHd / 2];
-#pragma unroll
-    for (int e = 0; e < kHd / 2; ++e) o2[e] = make_float2(0.f, 0.f);
+    float m = -INFINITY, l = 0.f;
     const bool live_t = t < ntq;
     const bool rows_live = live_t && q0 + t * kTileQ + quarter * 32 < nq;
     const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
-    auto fold = [&](int j) {                  // O'(t) of key tile j: both halves
-      mbar_wait(&sm.pv_full[t], j & 1);
-      tc_fence_after();
-      uint32_t ov[64];
-      tmem_ld32(tmem + lane_off + kOCol + 64 * t, ov);
-      tmem_ld32(tmem + lane_off + kOCol + 64 * t + 32, ov + 32);
-      tmem_wait_ld();
-      const float2 ap = make_float2(a_prev, a_prev);
-#pragma unroll
-      for (int e = 0; e < kHd / 2; ++e) {
-        const float2 d = fadd2(make_float2(__uint_as_float(ov[2 * e]), __uint_as_float(ov[2 * e + 1])),
-                               make_float2(__uint_as_float(ov[32 + 2 * e]),
-                                           __uint_as_float(ov[33 + 2 * e])));
-        o2[e] = ffma2(o2[e], ap, d);
-      }
-    };
+    // O(t) accumulates in TMEM over all key tiles (PV with enable-input from
+    // the second tile on); the softmax only waits for PV(j-1) before handing
+    // over P(j+1)... (bounds the p_full phases) and reads O once at the end
+    const uint32_t o_t = tmem + lane_off + kOCol + 64 * t;
     const bool tr = quarter == 0 && lane == 0;
     for (int j = 0; live_t && j < nkv; ++j) {
       const int n = j * ntq + t;
@@ -895,8 +880,6 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           tmem_st16(t_s + 64 * h + 48, pl + 16);
         }
         if (tr) NVREC_TR(t, j, 2 + 2 * h);
-        if (h == 0 && j > 0) fold(j - 1);
-        if (tr && h == 0) NVREC_TR(t, j, 3);
       }
       float2 sums = fadd2(sum2[0], sum2[1]);
       float tsum = sums.x + sums.y;
@@ -932,18 +915,49 @@ attn_x3w_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         tsum *= f;
         mn += k;
+        // O (all earlier tiles) by 2^(m - mn) once PV(j-1) has landed
+        mbar_wait(&sm.pv_full[t], (j - 1) & 1);
+        tc_fence_after();
+        const float al = ex2(m - mn);
+#pragma unroll 1
+        for (int g4 = 0; g4 < 2; ++g4) {
+          uint32_t ov[32];
+          tmem_ld32(o_t + 32 * g4, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * al);
+          tmem_st32(o_t + 32 * g4, ov);
+        }
       }
       const float alpha = ex2(m - mn);
       l = l * alpha + tsum;
       m = mn;
-      a_prev = alpha;
+      // P(j) goes to the issuer only once PV(j-1) is done: the issuer has then
+      // consumed p_full's previous phase (no parity aliasing), and a rescale
+      // above never races an in-flight PV
+      if (j > 0) {
+        mbar_wait(&sm.pv_full[t], (j - 1) & 1);
+        tc_fence_after();
+      }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
       if (tr) NVREC_TR(t, j, 5);
     }
     if (live_t) {
-      fold(nkv - 1);
+      mbar_wait(&sm.pv_full[t], (nkv - 1) & 1);
+      tc_fence_after();
+      float2 o2[kHd / 2];
+      {
+        uint32_t ov[64];
+        tmem_ld32(o_t, ov);
+        tmem_ld32(o_t + 32, ov + 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < kHd / 2; ++e)
+          o2[e] = fadd2(make_float2(__uint_as_float(ov[2 * e]), __uint_as_float(ov[2 * e + 1])),
+                        make_float2(__uint_as_float(ov[32 + 2 * e]), __uint_as_float(ov[33 + 2 * e])));
+      }
       const int q = q0 + t * kTileQ + row;
       if (q < nq && a.splits > 1) {
         float* dst = a.part + ((size_t(split) * a.seqs + seq) * a.ns + q) * kPart;

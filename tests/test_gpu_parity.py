@@ -284,6 +284,9 @@ def test_speculative_max_matches_exact_maxima(tmp_path, precision):
     assert np.array_equal(redo["out"], exact["out"])
     assert np.isfinite(spec["sharp"]).all()
     assert np.abs(spec["sharp"] - exact["sharp"]).max() <= TOL[precision]
+    # moderately sharp scores (in-kernel rescale of P and O, no overflow)
+    assert np.isfinite(spec["moderate"]).all()
+    assert np.abs(spec["moderate"] - exact["moderate"]).max() <= TOL[precision]
     # the sharp case overflows the speculative exponent: the exact fix-up
     # (a multi-CTA list walk) must have redone work items
     assert int(spec["redone"]) > 0
