@@ -9,7 +9,8 @@
 //   warp  8    TMA producer: Q tiles once, then K/V tiles through a 6-stage
 //              ring (K: 128 keys x 64 B, SWIZZLE_64B; V^T: 32 dims x 2 x 128 B,
 //              SWIZZLE_128B; the 3-D tensor maps zero-fill keys >= ns)
-//   warp  9    MMA issuer (one thread)
+//   warp  9    MMA issuer (lane 0; the split-operand variants: the whole warp,
+//              one lane elected per MMA, sm100.cuh mma_*_w)
 // TMEM (512 columns): every query tile owns two 128-column S buffers, so the
 // tensor core computes S(j+1) while the softmax warps work on S(j) -- the
 // softmax never waits for a QK^T round trip.  Key tile j of tile t:
@@ -677,10 +678,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
 // buffers: S tile n (query tile t = n % ntq, key tile j = n / ntq) lives in
 // buffer n % 3, and the MMA issuer runs PV two S tiles behind, i.e. the next S
 // of a query tile is issued as soon as the OTHER tile's previous P is done --
-// each softmax warpgroup finds its next S computed while it works.  O'(t) has
-// its own 64 columns (Ph [Vh | Vl] as one N = 64 MMA, then Pl Vh into the
-// first half; the fold adds the halves); TMEM = 3 x 128 + 2 x 64 = 512 columns.
-// Twice the keys per mbarrier round trip / O' fold of the 64-key variant.
+// each softmax warpgroup finds its next S computed while it works.  O(t) has
+// its own 64 columns and accumulates over ALL key tiles in TMEM (Ph [Vh | Vl]
+// as one N = 64 MMA, then Pl Vh into the first half; the halves are added once
+// at the end): with the speculative max, m only moves in the rare rescale,
+// which scales O in place.  TMEM = 3 x 128 + 2 x 64 = 512 columns.  The MMA
+// warp issues warp-wide (one elected lane per MMA).
 constexpr int kWTK = 128, kWStages = 4;
 #ifdef NVREC_TRACE
 // phase timestamps of one CTA (tools/trace_attn.py): role r (0: softmax warp
